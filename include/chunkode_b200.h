@@ -1,0 +1,233 @@
+/*
+ * chunkode_b200.h — C ABI of the B200-native chunked backward-Euler path.
+ *
+ * This is the drop-in boundary for the reference library `chunkode`
+ * (/root/reference/proj/core). The reference exposes the path as C++ free
+ * functions over an `OdeModel` virtual interface; a C++ shim keeps those
+ * signatures and forwards here. Every entry point below
+ * names the reference interface it replaces.
+ *
+ * Conventions:
+ *  - no exceptions cross this ABI; every call returns a cko_status and fills
+ *    a cko_error whose fields mirror the reference exception types
+ *    (/root/reference/proj/core/include/chunkode/errors.hpp:9-69);
+ *  - calls are synchronous on return;
+ *  - host arrays use the reference layouts: y0 (nb, n) row-major
+ *    (arrays.hpp:46-64), times (nt+1, nb) (time_grid.hpp:7-9), states
+ *    (nt+1, nb*n) (integrate.hpp:34-50), blocks (nc, nb, n, n) row-major
+ *    (arrays.hpp:103-131), chunk vectors (nc, nb, n) (arrays.hpp:66-101);
+ *  - `*_device` variants take device pointers in the same layouts (inputs
+ *    already resident in HBM) and run on the context's stream;
+ *  - one context per host thread; a context is bound to one CUDA device.
+ */
+#ifndef CHUNKODE_B200_H
+#define CHUNKODE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKO_ABI_VERSION 1
+
+/* Status codes: one per reference exception type (errors.hpp:9-69), plus
+ * device/communication failures the CPU library cannot have. */
+typedef enum {
+  CKO_OK = 0,
+  CKO_SHAPE_MISMATCH = 1,        /* ShapeMismatch        errors.hpp:14-16 */
+  CKO_SINGULAR_BLOCK = 2,        /* SingularBlock        errors.hpp:20-28 */
+  CKO_NEWTON_DIVERGENCE = 3,     /* NewtonDivergence     errors.hpp:48-64 */
+  CKO_NON_FINITE = 4,            /* NonFiniteOutput      errors.hpp:41-44 */
+  CKO_STRATEGY_UNAVAILABLE = 5,  /* StrategyUnavailable  errors.hpp:36-39 */
+  CKO_SIZE_GUARD = 6,            /* SizeGuardExceeded    errors.hpp:31-34 */
+  CKO_INVALID_TIME_GRID = 7,     /* InvalidTimeGrid      errors.hpp:67-69 */
+  CKO_ERROR = 8,                 /* plain chunkode::Error errors.hpp:9-11 */
+  CKO_CUDA = 9,                  /* CUDA runtime / launch failure */
+  CKO_COMM = 10                  /* multi-GPU exchange failure */
+} cko_status;
+
+/* Error payload. Field meanings follow the reference exceptions:
+ *  SingularBlock{chunk_index = row within the chunk, batch_index}
+ *  NewtonDivergence{chunk_start_step, batch_index (worst lane, integrate.cpp:167-174),
+ *                   iterations, residual_norm, initial_norm}
+ * batch_index is always a GLOBAL lane index (lane_offset applied). */
+typedef struct {
+  int code;
+  int chunk_index;
+  int batch_index;
+  int chunk_start_step;
+  int iterations;
+  double residual_norm;
+  double initial_norm;
+  char msg[256];
+} cko_error;
+
+/* WorkCounters (integrate.hpp:17-32): batched-call tallies. */
+typedef struct {
+  long long newton_iterations;
+  long long rate_evals;
+  long long jacobian_evals;
+  long long linear_solves;
+  long long reduction_sweeps;
+} cko_work;
+
+/* NewtonSettings (integrate.hpp:9-13). */
+typedef struct {
+  double tol_a; /* 1e-8 */
+  double tol_r; /* 1e-6 */
+  int max_iter; /* 100 */
+} cko_newton_settings;
+
+/* SolverChoice (linalg.hpp:89-95). */
+typedef enum { CKO_SOLVER_THOMAS = 0, CKO_SOLVER_PCR = 1, CKO_SOLVER_HYBRID = 2 } cko_solver_kind;
+typedef struct {
+  int kind;     /* cko_solver_kind */
+  int n_switch; /* hybrid reduction depth (default 1) */
+} cko_solver_choice;
+
+/* Device model kinds: device twins of the bundled reference models
+ * (models.hpp:14-41) plus the two models the benchmark configs add. */
+typedef enum {
+  CKO_MODEL_SCALAR_DECAY = 0,  /* models_simple.cpp:9-27   n=1, p=[p]                    */
+  CKO_MODEL_CONSTANT_RATE = 1, /* models_simple.cpp:29-45  n=1, p=[c]                    */
+  CKO_MODEL_LIN3 = 2,          /* SURVEY §8d C1            n=3, p=[A(3x3), f_a]          */
+  CKO_MODEL_MDS = 3,           /* models_mds.cpp:16-97     n=2u, p=[K(u),C(u),M(u),f_a,T(nb)] */
+  CKO_MODEL_CHABOCHE = 4,      /* models_chaboche.cpp:19-194 n=2+u,
+                                  p=[E,n,eta,s0,Kinf,tau,C(u),gamma(u),eps_a(nb),T]  */
+  CKO_MODEL_NODE = 5           /* models_node.cpp:13-205 (width = u+1) and the wide
+                                  variant: n=u, p=[W1(Wx(u+1)),b1(W),
+                                  W2(WxW),b2(W),W3(uxW),b3(u)]                        */
+} cko_model_kind;
+
+/* Flat model description, the C image of an OdeModel's identity:
+ * kind + dims + params() (ode_model.hpp:35). n_batch_model is the batch width
+ * the parameterisation was built for (OdeModel::n_batch, 0 = any);
+ * lane_offset maps local lane 0 to a global lane (batch sharding), so
+ * per-lane parameters (MDS T_b, Chaboche eps_a_b, NODE/LIN3 periods) are
+ * indexed by lane_offset + local lane. `params` is a host pointer. */
+typedef struct {
+  int kind;          /* cko_model_kind */
+  int n_unit;        /* MDS/Chaboche/NODE unit count; ignored otherwise */
+  int width;         /* NODE hidden width W (reference node: n_unit+1) */
+  int n_batch_model; /* parameterised batch width */
+  int lane_offset;   /* global lane index of local lane 0 */
+  int n_params;      /* length of params */
+  const double* params;
+} cko_model_desc;
+
+typedef struct cko_ctx cko_ctx;
+typedef struct cko_model cko_model;
+typedef struct cko_traj cko_traj;
+
+/* ---- context ------------------------------------------------------------ */
+int cko_abi_version(void);
+int cko_model_state_size(const cko_model_desc* desc);
+/* Parameter count the kind implies for (n_unit, width, n_batch_model). */
+int cko_model_param_count(const cko_model_desc* desc);
+
+/* Bind a context to CUDA device `device` with its own non-blocking stream. */
+cko_status cko_ctx_create(int device, cko_ctx** out, cko_error* err);
+cko_status cko_ctx_destroy(cko_ctx* ctx);
+/* Use an external stream (cudaStream_t) instead of the context's own. */
+cko_status cko_ctx_set_stream(cko_ctx* ctx, void* cuda_stream);
+/* Batch sharding: join a group of `world` ranks, one per GPU.
+ * `peer_flags` are this rank's view of every rank's exchange buffer (device
+ * pointers made accessible through CUDA IPC/P2P by the caller, world entries,
+ * each >= cko_comm_buffer_bytes()). With world == 1 sharding is off. */
+size_t cko_comm_buffer_bytes(void);
+cko_status cko_ctx_set_group(cko_ctx* ctx, int rank, int world, void* const* peer_buffers,
+                             cko_error* err);
+
+/* ---- models ------------------------------------------------------------- */
+/* Validate `desc` and upload its parameters to the device once.
+ * Replaces the per-call parameter walk of OdeModel::params()/eval_point
+ * (ode_model.hpp:103-128). Unknown kinds -> CKO_STRATEGY_UNAVAILABLE. */
+cko_status cko_model_create(cko_ctx* ctx, const cko_model_desc* desc, cko_model** out,
+                            cko_error* err);
+cko_status cko_model_destroy(cko_model* model);
+
+/* ---- integrator --------------------------------------------------------- */
+/* integrate_backward_euler (integrate.hpp:86-89, integrate.cpp:321-369).
+ * y0 (nb, n), times (nt+1, nb) are HOST arrays; the trajectory stays on the
+ * device (traj_out, may be NULL) and/or is copied to states_out (nt+1, nb*n)
+ * (may be NULL). `work` receives the forward WorkCounters. */
+cko_status cko_be_forward(cko_ctx* ctx, const cko_model* model, const double* y0,
+                          const double* times, int nb, int nt, int n_chunk,
+                          const cko_newton_settings* settings, const cko_solver_choice* solver,
+                          double* states_out, cko_traj** traj_out, cko_work* work,
+                          cko_error* err);
+
+/* Same, device pointers in and out (d_states: (nt+1, nb*n)). */
+cko_status cko_be_forward_device(cko_ctx* ctx, const cko_model* model, const double* d_y0,
+                                 const double* d_times, int nb, int nt, int n_chunk,
+                                 const cko_newton_settings* settings,
+                                 const cko_solver_choice* solver, double* d_states,
+                                 cko_work* work, cko_error* err);
+
+/* ---- adjoint ------------------------------------------------------------ */
+typedef enum { CKO_LOSS_FROBENIUS = 0, CKO_LOSS_USER = 1 } cko_loss_kind;
+
+/* adjoint_backward(..., Scheme::backward_euler, ...) (adjoint.hpp:63-66,
+ * adjoint.cpp:263-297) over a device trajectory. loss_kind FROBENIUS computes
+ * L = sqrt(sum_{step>=1} y^2) and dL/dy = y / L (adjoint.cpp:196-221);
+ * USER takes dL (nt+1, nb*n) from the host array dL_host (loss_out then
+ * receives NaN: the loss value belongs to the caller). grad_out (np) is a
+ * host array. */
+cko_status cko_be_adjoint(cko_ctx* ctx, const cko_model* model, const cko_traj* traj, int n_chunk,
+                          const cko_solver_choice* solver, int loss_kind, const double* dL_host,
+                          double* loss_out, double* grad_out, cko_work* bwd, cko_error* err);
+
+/* Same over a host trajectory: states (nt+1, nb*n), times (nt+1, nb). */
+cko_status cko_be_adjoint_host(cko_ctx* ctx, const cko_model* model, const double* states,
+                               const double* times, int nb, int nt, int n_chunk,
+                               const cko_solver_choice* solver, int loss_kind,
+                               const double* dL_host, double* loss_out, double* grad_out,
+                               cko_work* bwd, cko_error* err);
+
+/* Same, device pointers (d_dL may be NULL for FROBENIUS); grad_out is host. */
+cko_status cko_be_adjoint_device(cko_ctx* ctx, const cko_model* model, const double* d_states,
+                                 const double* d_times, int nb, int nt, int n_chunk,
+                                 const cko_solver_choice* solver, int loss_kind,
+                                 const double* d_dL, double* loss_out, double* grad_out,
+                                 cko_work* bwd, cko_error* err);
+
+/* gradient_adjoint (adjoint.hpp:76-80, adjoint.cpp:299-313) for the
+ * Frobenius loss: forward then adjoint, host buffers in and out. states_out
+ * may be NULL. */
+cko_status cko_gradient_adjoint(cko_ctx* ctx, const cko_model* model, const double* y0,
+                                const double* times, int nb, int nt, int n_chunk,
+                                const cko_newton_settings* settings,
+                                const cko_solver_choice* solver, double* states_out,
+                                double* loss_out, double* grad_out, cko_work* fwd, cko_work* bwd,
+                                cko_error* err);
+
+cko_status cko_traj_states(const cko_traj* traj, const double** d_states, int* nb, int* nt,
+                           int* n);
+cko_status cko_traj_destroy(cko_traj* traj);
+
+/* ---- block-bidiagonal solver -------------------------------------------- */
+/* solve_thomas / solve_pcr / solve_hybrid (linalg.hpp:55-81,
+ * linalg.cpp:307-344): diag (nc, nb, n, n), offdiag (nc-1, nb, n, n) or NULL
+ * for the -I couplings of the stepper (detail::solve_unit_offdiag,
+ * linalg.cpp:288-303); rhs (nc, nb, n) is overwritten by x. Host arrays.
+ * *sweeps receives the reduction sweep count (sum of e_i over partitions). */
+cko_status cko_block_bidiag_solve(cko_ctx* ctx, const cko_solver_choice* solver, int nc, int nb,
+                                  int n, const double* diag, const double* offdiag,
+                                  double* rhs_inout, long long* sweeps, cko_error* err);
+
+/* ---- single-chunk ops (integrate.hpp:53-77) ------------------------------ */
+/* newton_solve_chunk: dy (c, nb, n) in/out, y_start (nb, n), t_chunk and
+ * dt_chunk (c, nb); returns the iteration count in *iterations. */
+cko_status cko_newton_solve_chunk(cko_ctx* ctx, const cko_model* model, const double* y_start,
+                                  double* dy, const double* t_chunk, const double* dt_chunk,
+                                  int c, int nb, const cko_newton_settings* settings,
+                                  const cko_solver_choice* solver, int chunk_start_step,
+                                  int* iterations, cko_work* work, cko_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHUNKODE_B200_H */
