@@ -1,0 +1,396 @@
+"""Python mirror of the reference chunkode API for the backward-Euler path.
+
+Same names, argument meanings and error behaviour as
+/root/reference/proj/core/include/chunkode/{time_grid,integrate,adjoint,linalg}.hpp;
+every call runs on the GPU through the C ABI (include/chunkode_b200.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import abi
+from ._native import lib
+from .abi import dptr
+from .errors import Error, InvalidTimeGrid, ShapeMismatch, raise_for
+from .models import Model
+
+
+# ---------------------------------------------------------------------------
+# settings and counters (integrate.hpp:9-32, linalg.hpp:89-95)
+# ---------------------------------------------------------------------------
+class SolverKind:
+    thomas = abi.CKO_SOLVER_THOMAS
+    pcr = abi.CKO_SOLVER_PCR
+    hybrid = abi.CKO_SOLVER_HYBRID
+
+
+_KIND_BY_NAME = {"thomas": 0, "pcr": 1, "hybrid": 2}
+
+
+@dataclass
+class SolverChoice:
+    kind: int = SolverKind.thomas
+    n_switch: int = 1
+
+    def c(self) -> abi.CkoSolverChoice:
+        k = _KIND_BY_NAME[self.kind] if isinstance(self.kind, str) else int(self.kind)
+        return abi.CkoSolverChoice(k, int(self.n_switch))
+
+
+@dataclass
+class NewtonSettings:
+    tol_a: float = 1e-8
+    tol_r: float = 1e-6
+    max_iter: int = 100
+
+    def c(self) -> abi.CkoNewtonSettings:
+        return abi.CkoNewtonSettings(float(self.tol_a), float(self.tol_r), int(self.max_iter))
+
+
+@dataclass
+class WorkCounters:
+    newton_iterations: int = 0
+    rate_evals: int = 0
+    jacobian_evals: int = 0
+    linear_solves: int = 0
+    reduction_sweeps: int = 0
+
+    @classmethod
+    def from_c(cls, w: abi.CkoWork) -> "WorkCounters":
+        return cls(*(int(getattr(w, k)) for k, _ in abi.CkoWork._fields_))
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+    def __iadd__(self, o):
+        for k in self.__dict__:
+            setattr(self, k, getattr(self, k) + getattr(o, k))
+        return self
+
+
+# ---------------------------------------------------------------------------
+# time grid (time_grid.hpp:10-28, time_grid.cpp:7-29)
+# ---------------------------------------------------------------------------
+class TimeGrid:
+    def __init__(self, times):
+        t = np.ascontiguousarray(times, dtype=np.float64)
+        if t.ndim != 2 or t.shape[0] < 2 or t.shape[1] < 1:
+            raise InvalidTimeGrid("time grid needs at least one step and one batch lane")
+        bad = ~(t[1:] > t[:-1])
+        if bad.any():
+            i, b = np.argwhere(bad)[0]
+            raise InvalidTimeGrid(f"time grid must be strictly increasing (step {i + 1}, batch {b})")
+        self._t = t
+
+    @staticmethod
+    def uniform(n_time: int, n_batch: int, t_max: float) -> "TimeGrid":
+        if n_time < 1 or n_batch < 1:
+            raise InvalidTimeGrid("uniform grid needs n_time, n_batch >= 1")
+        ti = np.array([t_max * float(i) / float(n_time) for i in range(n_time + 1)])
+        return TimeGrid(np.repeat(ti[:, None], n_batch, axis=1))
+
+    @property
+    def n_time(self) -> int:
+        return self._t.shape[0] - 1
+
+    @property
+    def n_batch(self) -> int:
+        return self._t.shape[1]
+
+    @property
+    def times(self) -> np.ndarray:
+        return self._t
+
+    def time(self, step: int, b: int) -> float:
+        return float(self._t[step, b])
+
+    def dt(self, step: int, b: int) -> float:
+        return float(self._t[step, b] - self._t[step - 1, b])
+
+
+@dataclass
+class Trajectory:
+    """integrate.hpp:34-50: states (n_time + 1, n_batch * n_size)."""
+
+    states: np.ndarray
+    grid: TimeGrid
+    n_batch: int
+    n_size: int
+    work: WorkCounters = field(default_factory=WorkCounters)
+
+    @property
+    def n_time(self) -> int:
+        return self.states.shape[0] - 1
+
+    def point(self, step: int, b: int) -> np.ndarray:
+        return self.states[step, b * self.n_size:(b + 1) * self.n_size]
+
+
+@dataclass
+class LossSpec:
+    """adjoint.hpp:14-20. value(traj) -> float, state_gradient(traj) -> array shaped like traj.states.
+    frobenius=True selects the fused device Frobenius loss."""
+
+    value: Optional[Callable] = None
+    state_gradient: Optional[Callable] = None
+    frobenius: bool = False
+
+
+def loss_frobenius() -> LossSpec:
+    """adjoint.cpp:196-221: sqrt of the sum of squares over steps 1..n_time."""
+    def value(tr):
+        return float(np.sqrt(np.sum(tr.states[1:] ** 2)))
+
+    def grad(tr):
+        L = value(tr)
+        g = np.zeros_like(tr.states)
+        if L > 0:
+            g[1:] = tr.states[1:] / L
+        return g
+
+    return LossSpec(value, grad, frobenius=True)
+
+
+@dataclass
+class GradientResult:
+    loss: float
+    gradient: np.ndarray
+    trajectory: Trajectory
+    backward_work: WorkCounters
+
+
+# ---------------------------------------------------------------------------
+# device context + model cache
+# ---------------------------------------------------------------------------
+class Context:
+    """cko_ctx: one CUDA device, one stream, a workspace pool."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        e = abi.CkoError()
+        raise_for(lib().cko_ctx_create(device, C.byref(h), C.byref(e)), e)
+        self.h = h
+        self._models: dict = {}
+
+    def close(self):
+        for dm in self._models.values():
+            lib().cko_model_destroy(dm)
+        self._models.clear()
+        if self.h:
+            lib().cko_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int):
+        lib().cko_ctx_set_stream(self.h, C.c_void_p(stream_handle))
+
+    def model(self, m: Model) -> C.c_void_p:
+        key = (m.kind, m.n_unit, m.width, m.n_batch, m.lane_offset, m.params.tobytes())
+        dm = self._models.get(key)
+        if dm is None:
+            dm = C.c_void_p()
+            e = abi.CkoError()
+            d = m.desc()
+            raise_for(lib().cko_model_create(self.h, C.byref(d), C.byref(dm), C.byref(e)), e)
+            if len(self._models) > 64:
+                for v in self._models.values():
+                    lib().cko_model_destroy(v)
+                self._models.clear()
+            self._models[key] = dm
+        return dm
+
+
+_tls = threading.local()
+
+
+def default_context(device: int = 0) -> Context:
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    if device not in ctxs:
+        ctxs[device] = Context(device)
+    return ctxs[device]
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# integrator / adjoint (integrate.hpp:86-89, adjoint.hpp:63-80)
+# ---------------------------------------------------------------------------
+def integrate_backward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int,
+                             settings: NewtonSettings | None = None, solver: SolverChoice | None = None,
+                             ctx: Context | None = None) -> Trajectory:
+    settings = settings or NewtonSettings()
+    solver = solver or SolverChoice()
+    y0 = _f64(y0)
+    if y0.ndim != 2 or y0.shape[1] != model.state_size:
+        raise ShapeMismatch("integrate: y0 width != state size")
+    if y0.shape[0] != grid.n_batch:
+        raise ShapeMismatch("integrate: y0 rows != grid batch width")
+    ctx = ctx or default_context()
+    nb, nt, n = grid.n_batch, grid.n_time, model.state_size
+    states = np.zeros((nt + 1, nb * n))
+    w, e = abi.CkoWork(), abi.CkoError()
+    st, sv = settings.c(), solver.c()
+    rc = lib().cko_be_forward(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
+                              C.byref(st), C.byref(sv), dptr(states), None, C.byref(w), C.byref(e))
+    raise_for(rc, e)
+    return Trajectory(states, grid, nb, n, WorkCounters.from_c(w))
+
+
+def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpec | None = None,
+                     solver: SolverChoice | None = None, work: WorkCounters | None = None,
+                     ctx: Context | None = None):
+    """Returns (loss, gradient) like adjoint.hpp:63-66; `work` (if given) receives the backward counters."""
+    loss = loss or loss_frobenius()
+    solver = solver or SolverChoice()
+    if traj.n_size != model.state_size:
+        raise ShapeMismatch("adjoint: trajectory width != model size")
+    if n_chunk < 1:
+        raise ShapeMismatch("adjoint: n_chunk must be >= 1")
+    if loss.value is None or loss.state_gradient is None:
+        raise ShapeMismatch("loss: both callbacks must be set")
+    ctx = ctx or default_context()
+    grad = np.zeros(model.params.size)
+    L = C.c_double(0.0)
+    w, e = abi.CkoWork(), abi.CkoError()
+    sv = solver.c()
+    if loss.frobenius:
+        kind, dL = abi.CKO_LOSS_FROBENIUS, None
+    else:
+        kind = abi.CKO_LOSS_USER
+        dL = _f64(loss.state_gradient(traj))
+        if dL.shape != traj.states.shape:
+            raise ShapeMismatch("loss gradient: output must be shaped like the trajectory states")
+    rc = lib().cko_be_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
+                                   traj.n_batch, traj.n_time, int(n_chunk), C.byref(sv), kind, dptr(dL),
+                                   C.byref(L), dptr(grad), C.byref(w), C.byref(e))
+    raise_for(rc, e)
+    if work is not None:
+        work += WorkCounters.from_c(w)
+    Lv = L.value if loss.frobenius else float(loss.value(traj))
+    return Lv, grad
+
+
+def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossSpec | None = None,
+                     solver: SolverChoice | None = None, settings: NewtonSettings | None = None,
+                     ctx: Context | None = None) -> GradientResult:
+    """adjoint.cpp:299-313; the Frobenius loss runs fully on the device."""
+    loss = loss or loss_frobenius()
+    settings = settings or NewtonSettings()
+    solver = solver or SolverChoice()
+    if not loss.frobenius:
+        tr = integrate_backward_euler(model, y0, grid, n_chunk, settings, solver, ctx)
+        bw = WorkCounters()
+        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx)
+        return GradientResult(L, g, tr, bw)
+    y0 = _f64(y0)
+    if y0.ndim != 2 or y0.shape[1] != model.state_size or y0.shape[0] != grid.n_batch:
+        raise ShapeMismatch("integrate: y0 shape does not match the model / grid")
+    ctx = ctx or default_context()
+    nb, nt, n = grid.n_batch, grid.n_time, model.state_size
+    states = np.zeros((nt + 1, nb * n))
+    grad = np.zeros(model.params.size)
+    L = C.c_double(0.0)
+    wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+    st, sv = settings.c(), solver.c()
+    rc = lib().cko_gradient_adjoint(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
+                                    C.byref(st), C.byref(sv), dptr(states), C.byref(L), dptr(grad), C.byref(wf),
+                                    C.byref(wb), C.byref(e))
+    raise_for(rc, e)
+    tr = Trajectory(states, grid, nb, n, WorkCounters.from_c(wf))
+    return GradientResult(L.value, grad, tr, WorkCounters.from_c(wb))
+
+
+def newton_solve_chunk(model: Model, y_start, dy, t_chunk, dt_chunk, settings: NewtonSettings | None = None,
+                       solver: SolverChoice | None = None, work: WorkCounters | None = None,
+                       chunk_start_step: int = 1, ctx: Context | None = None):
+    """integrate.hpp:63-67: dy (c, nb, n) updated in place; returns the iteration count."""
+    settings = settings or NewtonSettings()
+    solver = solver or SolverChoice()
+    ctx = ctx or default_context()
+    y_start = _f64(y_start)
+    t_chunk, dt_chunk = _f64(t_chunk), _f64(dt_chunk)
+    c, nb = t_chunk.shape
+    buf = _f64(dy).copy()
+    it = C.c_int(0)
+    w, e = abi.CkoWork(), abi.CkoError()
+    st, sv = settings.c(), solver.c()
+    rc = lib().cko_newton_solve_chunk(ctx.h, ctx.model(model), dptr(y_start), dptr(buf), dptr(t_chunk),
+                                      dptr(dt_chunk), c, nb, C.byref(st), C.byref(sv), int(chunk_start_step),
+                                      C.byref(it), C.byref(w), C.byref(e))
+    raise_for(rc, e)
+    dy[...] = buf
+    if work is not None:
+        work += WorkCounters.from_c(w)
+    return int(it.value)
+
+
+# ---------------------------------------------------------------------------
+# block-bidiagonal solvers (linalg.hpp:19-87)
+# ---------------------------------------------------------------------------
+@dataclass
+class BlockBidiagonalSystem:
+    diag: np.ndarray       # (nc, nb, n, n)
+    offdiag: np.ndarray    # (nc - 1, nb, n, n)
+
+    @classmethod
+    def zeros(cls, n_chunk, n_batch, n_size):
+        return cls(np.zeros((n_chunk, n_batch, n_size, n_size)),
+                   np.zeros((max(n_chunk - 1, 0), n_batch, n_size, n_size)))
+
+
+def _solve(sys_diag, sys_off, rhs, solver: SolverChoice, unit: bool, ctx: Context | None):
+    ctx = ctx or default_context()
+    diag = _f64(sys_diag)
+    if diag.ndim != 4 or diag.shape[2] != diag.shape[3]:
+        raise ShapeMismatch("block bidiagonal system must be non-empty")
+    nc, nb, n, _ = diag.shape
+    x = _f64(rhs).copy()
+    if x.shape != (nc, nb, n):
+        raise ShapeMismatch("right-hand side shape must match the system")
+    off = None
+    if not unit:
+        off = _f64(sys_off)
+        if nc > 1 and off.shape != (nc - 1, nb, n, n):
+            raise ShapeMismatch("off-diagonal block array must be (n_chunk-1, n_batch, n_size, n_size)")
+    sw = C.c_longlong(0)
+    e = abi.CkoError()
+    sv = solver.c()
+    rc = lib().cko_block_bidiag_solve(ctx.h, C.byref(sv), nc, nb, n, dptr(diag),
+                                      dptr(off) if off is not None else None, dptr(x), C.byref(sw), C.byref(e))
+    raise_for(rc, e)
+    return x, int(sw.value)
+
+
+def solve_thomas(sys: BlockBidiagonalSystem, rhs, ctx=None) -> np.ndarray:
+    return _solve(sys.diag, sys.offdiag, rhs, SolverChoice(SolverKind.thomas), False, ctx)[0]
+
+
+def solve_pcr(sys: BlockBidiagonalSystem, rhs, ctx=None):
+    """Returns (x, sweep_count) — sweep_count is the reference's out-parameter."""
+    return _solve(sys.diag, sys.offdiag, rhs, SolverChoice(SolverKind.pcr), False, ctx)
+
+
+def solve_hybrid(sys: BlockBidiagonalSystem, rhs, n_switch: int, ctx=None):
+    if n_switch < 0:
+        raise Error("solve_hybrid: n_switch must be >= 0")
+    return _solve(sys.diag, sys.offdiag, rhs, SolverChoice(SolverKind.hybrid, n_switch), False, ctx)
+
+
+def solve_unit_offdiag(diag, rhs, solver: SolverChoice, ctx=None):
+    """detail::solve_unit_offdiag (linalg.cpp:288-303): couplings exactly -I."""
+    return _solve(diag, None, rhs, solver, True, ctx)

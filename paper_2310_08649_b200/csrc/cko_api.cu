@@ -1,0 +1,770 @@
+// cko_api.cu — host implementation of the C ABI in include/chunkode_b200.h.
+//
+// Owns CUDA resources (stream, grow-only workspace pool, model parameter
+// uploads, device trajectories), validates arguments like the reference
+// (ShapeMismatch / InvalidTimeGrid checks of integrate.cpp:12-21, 257-265,
+// time_grid.cpp:7-19, linalg.cpp:86-98), launches the kernels of
+// cko_kernels.cu and maps device status words back to the reference error
+// types (errors.hpp:9-69). No CPU fallback exists: without a usable CUDA
+// device every entry point returns CKO_CUDA.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/chunkode_b200.h"
+#include "cko_kernels.cuh"
+
+using namespace cko;
+
+namespace {
+
+cko_status fail(cko_error* e, cko_status code, const char* fmt, ...) {
+  if (e) {
+    std::memset(e, 0, sizeof(*e));
+    e->code = code;
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(e->msg, sizeof e->msg, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+
+cko_status ok(cko_error* e) {
+  if (e) std::memset(e, 0, sizeof(*e));
+  return CKO_OK;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(err, CKO_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));        \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&p, b < 256 ? 256 : b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int state_size(const cko_model_desc* d) {
+  switch (d->kind) {
+    case CKO_MODEL_SCALAR_DECAY:
+    case CKO_MODEL_CONSTANT_RATE: return 1;
+    case CKO_MODEL_LIN3: return 3;
+    case CKO_MODEL_MDS: return d->n_unit >= 1 ? 2 * d->n_unit : -1;
+    case CKO_MODEL_CHABOCHE: return d->n_unit >= 1 ? 2 + d->n_unit : -1;
+    case CKO_MODEL_NODE: return d->n_unit >= 1 ? d->n_unit : -1;
+  }
+  return -1;
+}
+
+int param_count(const cko_model_desc* d) {
+  const int u = d->n_unit, W = d->width, nb = d->n_batch_model;
+  switch (d->kind) {
+    case CKO_MODEL_SCALAR_DECAY:
+    case CKO_MODEL_CONSTANT_RATE: return 1;
+    case CKO_MODEL_LIN3: return 10;
+    case CKO_MODEL_MDS: return 3 * u + 1 + nb;
+    case CKO_MODEL_CHABOCHE: return 6 + 2 * u + nb + 1;
+    case CKO_MODEL_NODE: return W * (u + 1) + W + W * W + W + u * W + u;
+  }
+  return -1;
+}
+
+// chunkode::linspace (linalg.cpp:386-396), bit-exact.
+std::vector<double> linspace(double lo, double hi, int n) {
+  std::vector<double> v(n > 0 ? n : 0);
+  if (n <= 0) return v;
+  if (n == 1) {
+    v[0] = lo;
+    return v;
+  }
+  for (int i = 0; i < n; ++i) v[i] = lo + (hi - lo) * double(i) / double(n - 1);
+  v[n - 1] = hi;
+  return v;
+}
+
+// Reduction sweeps of one solve of a c-row chunk (linalg.cpp:203-254).
+long long sweeps_of(int c, int kind, int n_switch) {
+  if (kind == CKO_SOLVER_THOMAS) return 0;
+  long long s = 0;
+  for (int bit = 30; bit >= 0; --bit) {
+    const int m = 1 << bit;
+    if (!(c & m)) continue;
+    int e = 0;
+    while ((1 << e) < m) ++e;
+    s += kind == CKO_SOLVER_PCR ? e : (n_switch < e ? n_switch : e);
+  }
+  return s;
+}
+
+}  // namespace
+
+struct cko_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sms = 0;
+  // workspace pool
+  Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad;
+  Buf h_y0, h_times, h_states, h_dL, h_rhs, h_diag, h_off;  // staging for host-buffer calls
+  std::vector<int> iters_host;
+  // batch sharding
+  GroupView grp{};
+};
+
+struct cko_model {
+  cko_ctx* ctx = nullptr;
+  cko_model_desc desc{};
+  DevModel dm{};
+  double* d_params = nullptr;
+  double* d_periods = nullptr;
+};
+
+struct cko_traj {
+  cko_ctx* ctx = nullptr;
+  double* d_states = nullptr;
+  double* d_times = nullptr;
+  int nb = 0, nt = 0, n = 0;
+};
+
+extern "C" {
+
+int cko_abi_version(void) { return CKO_ABI_VERSION; }
+int cko_model_state_size(const cko_model_desc* d) { return d ? state_size(d) : -1; }
+int cko_model_param_count(const cko_model_desc* d) { return d ? param_count(d) : -1; }
+size_t cko_comm_buffer_bytes(void) { return sizeof(unsigned long long) * 2 * 8; }
+
+cko_status cko_ctx_create(int device, cko_ctx** out, cko_error* err) {
+  if (!out) return fail(err, CKO_ERROR, "cko_ctx_create: null output");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(err, CKO_CUDA, "no CUDA device available (%s): the B200 path has no CPU fallback",
+                e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  if (device < 0 || device >= count) return fail(err, CKO_CUDA, "CUDA device %d out of range", device);
+  CUDA_TRY(cudaSetDevice(device));
+  cko_ctx* c = new (std::nothrow) cko_ctx();
+  if (!c) return fail(err, CKO_ERROR, "out of host memory");
+  c->device = device;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(err, CKO_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  }
+  c->own_stream = true;
+  c->grp.rank = 0;
+  c->grp.world = 1;
+  e = c->gs.ensure(sizeof(GridSync));
+  if (e == cudaSuccess) e = cudaMemset(c->gs.p, 0, sizeof(GridSync));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(err, CKO_CUDA, "workspace: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return ok(err);
+}
+
+cko_status cko_ctx_destroy(cko_ctx* c) {
+  if (!c) return CKO_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (Buf* b : {&c->slab, &c->piv, &c->rn, &c->r0, &c->iters, &c->gs, &c->key, &c->info, &c->loss,
+                 &c->scratch, &c->lambda, &c->wq, &c->vjp, &c->grad, &c->h_y0, &c->h_times,
+                 &c->h_states, &c->h_dL, &c->h_rhs, &c->h_diag, &c->h_off})
+    b->release();
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return CKO_OK;
+}
+
+cko_status cko_ctx_set_stream(cko_ctx* c, void* s) {
+  if (!c) return CKO_ERROR;
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  c->stream = static_cast<cudaStream_t>(s);
+  c->own_stream = false;
+  return CKO_OK;
+}
+
+cko_status cko_ctx_set_group(cko_ctx* c, int rank, int world, void* const* peers, cko_error* err) {
+  if (!c) return fail(err, CKO_ERROR, "null context");
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    return fail(err, CKO_ERROR, "cko_ctx_set_group: need 1 <= world <= 8, 0 <= rank < world");
+  c->grp.rank = rank;
+  c->grp.world = world;
+  for (int r = 0; r < 8; ++r)
+    c->grp.peer_slots[r] = (world > 1 && r < world) ? static_cast<unsigned long long*>(peers[r]) : nullptr;
+  return ok(err);
+}
+
+cko_status cko_model_create(cko_ctx* c, const cko_model_desc* d, cko_model** out, cko_error* err) {
+  if (!c || !d || !out) return fail(err, CKO_ERROR, "cko_model_create: null argument");
+  *out = nullptr;
+  const int n = state_size(d);
+  if (n < 1 || d->kind < 0 || d->kind > CKO_MODEL_NODE)
+    return fail(err, CKO_STRATEGY_UNAVAILABLE, "model kind %d has no device twin", d->kind);
+  const bool lane_model = d->kind != CKO_MODEL_SCALAR_DECAY && d->kind != CKO_MODEL_CONSTANT_RATE;
+  if (lane_model && d->n_batch_model < 1)
+    return fail(err, CKO_SHAPE_MISMATCH, "model needs n_batch_model >= 1");
+  if (d->kind == CKO_MODEL_NODE && (d->width < 1 || d->width > NODE_MAX_W || n > NODE_MAX_N))
+    return fail(err, CKO_STRATEGY_UNAVAILABLE,
+                "neural ODE width %d / state %d exceeds the point-wise device kernels (W <= %d, n <= %d)",
+                d->width, n, NODE_MAX_W, NODE_MAX_N);
+  const int np = param_count(d);
+  if (np != d->n_params || !d->params)
+    return fail(err, CKO_SHAPE_MISMATCH, "parameter count %d does not match the model (%d)", d->n_params, np);
+  CUDA_TRY(cudaSetDevice(c->device));
+  cko_model* m = new (std::nothrow) cko_model();
+  if (!m) return fail(err, CKO_ERROR, "out of host memory");
+  m->ctx = c;
+  m->desc = *d;
+  m->desc.params = nullptr;
+  cudaError_t e = cudaMalloc(&m->d_params, sizeof(double) * np);
+  if (e == cudaSuccess) e = cudaMemcpy(m->d_params, d->params, sizeof(double) * np, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && lane_model) {
+    const auto per = linspace(1e-2, 1.0, d->n_batch_model);
+    e = cudaMalloc(&m->d_periods, sizeof(double) * per.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(m->d_periods, per.data(), sizeof(double) * per.size(), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    cudaFree(m->d_params);
+    cudaFree(m->d_periods);
+    delete m;
+    return fail(err, CKO_CUDA, "model upload: %s", cudaGetErrorString(e));
+  }
+  DevModel& dm = m->dm;
+  dm.kind = d->kind;
+  dm.n = n;
+  dm.nu = d->n_unit;
+  dm.W = d->width;
+  dm.nbm = d->n_batch_model;
+  dm.off = d->lane_offset;
+  dm.np = np;
+  dm.p = m->d_params;
+  dm.periods = m->d_periods;
+  *out = m;
+  return ok(err);
+}
+
+cko_status cko_model_destroy(cko_model* m) {
+  if (!m) return CKO_OK;
+  cudaSetDevice(m->ctx->device);
+  cudaFree(m->d_params);
+  cudaFree(m->d_periods);
+  delete m;
+  return CKO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+cko_status check_lanes(const cko_model* m, int nb, cko_error* err) {
+  const bool lane_model = m->desc.kind != CKO_MODEL_SCALAR_DECAY && m->desc.kind != CKO_MODEL_CONSTANT_RATE;
+  if (lane_model && m->desc.lane_offset + nb > m->desc.n_batch_model)
+    return fail(err, CKO_SHAPE_MISMATCH, "integrate: model batch width != y0 rows");
+  return CKO_OK;
+}
+
+cko_status check_grid_host(const double* times, int nt, int nb, cko_error* err) {
+  if (nt < 1 || nb < 1)
+    return fail(err, CKO_INVALID_TIME_GRID, "time grid needs at least one step and one batch lane");
+  for (int i = 1; i <= nt; ++i)
+    for (int b = 0; b < nb; ++b)
+      if (!(times[(size_t)i * nb + b] > times[(size_t)(i - 1) * nb + b]))
+        return fail(err, CKO_INVALID_TIME_GRID, "time grid must be strictly increasing (step %d, batch %d)", i, b);
+  return CKO_OK;
+}
+
+cko_status prepare_slab(cko_ctx* c, int G, int nb, int nc, int n, bool pcr, Slab& s, cko_error* err) {
+  const int Lmax = (nb + G - 1) / G;
+  s.Lmax = Lmax;
+  s.Pmax = nc * Lmax;
+  s.doubles = (size_t)s.Pmax * slab_doubles_per_point(n, pcr);
+  s.ints = (size_t)s.Pmax * n;
+  CUDA_TRY(c->slab.ensure(sizeof(double) * s.doubles * G));
+  CUDA_TRY(c->piv.ensure(sizeof(int) * s.ints * G));
+  s.base = c->slab.as<double>();
+  s.pbase = c->piv.as<int>();
+  return CKO_OK;
+}
+
+constexpr int kThreads = 256;
+
+// Core forward on device buffers (states row 0 must hold y0).
+cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
+                        int nc, const cko_newton_settings* st, const cko_solver_choice* sv, const double* d_dy,
+                        cko_work* work, int* iters_out, cko_error* err) {
+  if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
+  if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
+  if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
+  if (sv->kind == CKO_SOLVER_HYBRID && sv->n_switch < 0)
+    return fail(err, CKO_ERROR, "solve_hybrid: n_switch must be >= 0");
+  if (cko_status s = check_lanes(m, nb, err)) return s;
+  const int n = m->dm.n;
+  const int nc_eff = nc < nt ? nc : nt;
+  const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
+  int maxg = forward_max_grid(m->dm.kind, kThreads, c->device);
+  if (maxg < 1) return fail(err, CKO_CUDA, "forward kernel cannot be made resident");
+  const int G = nb < maxg ? nb : maxg;
+  Slab slab;
+  if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  const int n_chunks = (nt + nc - 1) / nc;
+  CUDA_TRY(c->rn.ensure(sizeof(double) * nb));
+  CUDA_TRY(c->r0.ensure(sizeof(double) * nb));
+  CUDA_TRY(c->iters.ensure(sizeof(int) * n_chunks));
+  CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(c->info.ensure(sizeof(int) * 4));
+  CUDA_TRY(cudaMemsetAsync(c->gs.p, 0, offsetof(GridSync, ext_gen), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->info.p, 0, sizeof(int) * 4, c->stream));
+  FwdLaunch a{};
+  a.m = m->dm;
+  a.states = d_states;
+  a.times = d_times;
+  a.dy_init = d_dy;
+  a.nb = nb;
+  a.nt = nt;
+  a.nc = nc;
+  a.tol_a = st->tol_a;
+  a.tol_r = st->tol_r;
+  a.max_iter = st->max_iter;
+  a.solver = sv->kind;
+  a.n_switch = sv->n_switch;
+  a.slab = slab;
+  a.rn = c->rn.as<double>();
+  a.r0 = c->r0.as<double>();
+  a.iters = c->iters.as<int>();
+  a.gs = c->gs.as<GridSync>();
+  a.grp = c->grp;
+  a.sing_key = c->key.as<unsigned long long>();
+  a.info = c->info.as<int>();
+  a.budget_ns = 60ull * 1000 * 1000 * 1000;
+  a.grid = G;
+  a.threads = kThreads;
+  CUDA_TRY(launch_forward(a, c->stream));
+  int info[4];
+  unsigned long long key;
+  CUDA_TRY(cudaMemcpyAsync(info, c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
+  c->iters_host.resize(n_chunks);
+  CUDA_TRY(cudaMemcpyAsync(c->iters_host.data(), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int off = m->desc.lane_offset;
+  if (info[0] == 4) return fail(err, CKO_COMM, "grid barrier timed out (device or peer stalled)");
+  if (info[0] == 1) {
+    const int k = (int)(key / (unsigned long long)nb), b = (int)(key % (unsigned long long)nb);
+    cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block at chunk row %d, batch %d", k, b + off);
+    if (err) err->chunk_index = k, err->batch_index = b + off;
+    return s;
+  }
+  if (info[0] == 2) {
+    std::vector<double> rn(nb), r0(nb);
+    CUDA_TRY(cudaMemcpy(rn.data(), c->rn.p, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(r0.data(), c->r0.p, sizeof(double) * nb, cudaMemcpyDeviceToHost));
+    int w = 0;  // worst_lane (integrate.cpp:167-174)
+    for (int b = 0; b < nb; ++b) {
+      if (!std::isfinite(rn[b])) {
+        w = b;
+        break;
+      }
+      if (rn[b] > rn[w]) w = b;
+    }
+    cko_status s = fail(err, CKO_NEWTON_DIVERGENCE,
+                        "Newton did not converge for chunk starting at step %d (batch %d): |r| = %g after %d "
+                        "iterations, |r0| = %g",
+                        info[1], w + off, rn[w], info[2], r0[w]);
+    if (err) {
+      err->chunk_start_step = info[1];
+      err->batch_index = w + off;
+      err->iterations = info[2];
+      err->residual_norm = rn[w];
+      err->initial_norm = r0[w];
+    }
+    return s;
+  }
+  if (info[3] != n_chunks) return fail(err, CKO_CUDA, "forward kernel stopped after %d of %d chunks", info[3], n_chunks);
+  if (work) {
+    std::memset(work, 0, sizeof(*work));
+    for (int j = 0; j < n_chunks; ++j) {
+      const int cj = (j == n_chunks - 1) ? nt - j * nc : nc;
+      const int it = c->iters_host[j];
+      work->newton_iterations += it;
+      work->rate_evals += it + 1;
+      work->jacobian_evals += it;
+      work->linear_solves += it;
+      work->reduction_sweeps += (long long)it * sweeps_of(cj, sv->kind, sv->n_switch);
+    }
+  }
+  if (iters_out) *iters_out = c->iters_host.empty() ? 0 : c->iters_host[0];
+  return ok(err);
+}
+
+// Core adjoint on device buffers.
+cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times, int nb,
+                        int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* d_dL,
+                        double* loss_out, double* grad_out, cko_work* bwd, cko_error* err) {
+  if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
+  if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
+  if (sv->kind == CKO_SOLVER_HYBRID && sv->n_switch < 0)
+    return fail(err, CKO_ERROR, "solve_hybrid: n_switch must be >= 0");
+  if (loss_kind == CKO_LOSS_USER && !d_dL) return fail(err, CKO_ERROR, "user loss needs dL");
+  if (cko_status s = check_lanes(m, nb, err)) return s;
+  const int n = m->dm.n, np = m->dm.np;
+  const int nc_eff = nc < nt ? nc : nt;
+  const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
+  const int G = nb < 2 * c->sms ? nb : 2 * c->sms;
+  Slab slab;
+  if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  const size_t row = (size_t)nb * n;
+  CUDA_TRY(c->lambda.ensure(sizeof(double) * row));
+  CUDA_TRY(c->wq.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(c->loss.ensure(sizeof(double)));
+  CUDA_TRY(c->scratch.ensure(sizeof(double) * 1024));
+  CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm)));
+  CUDA_TRY(c->grad.ensure(sizeof(double) * np));
+  CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+  if (loss_kind == CKO_LOSS_FROBENIUS)
+    CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->stream));
+  AdjLaunch a{};
+  a.m = m->dm;
+  a.states = d_states;
+  a.times = d_times;
+  a.dL = loss_kind == CKO_LOSS_USER ? d_dL : nullptr;
+  a.loss = loss_kind == CKO_LOSS_USER ? nullptr : c->loss.as<double>();
+  a.nb = nb;
+  a.nt = nt;
+  a.nc = nc;
+  a.solver = sv->kind;
+  a.n_switch = sv->n_switch;
+  a.slab = slab;
+  a.lambda = c->lambda.as<double>();
+  a.wq = c->wq.as<double>();
+  a.sing_key = c->key.as<unsigned long long>();
+  a.grid = G;
+  a.threads = kThreads;
+  CUDA_TRY(launch_adjoint(a, c->stream));
+  CUDA_TRY(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),
+                      c->grad.as<double>(), c->stream));
+  unsigned long long key;
+  double L = NAN;
+  CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
+  if (loss_kind == CKO_LOSS_FROBENIUS)
+    CUDA_TRY(cudaMemcpyAsync(&L, c->loss.p, sizeof L, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(grad_out, c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int off = m->desc.lane_offset;
+  if (key != ~0ull) {
+    const int b = (int)(key % (unsigned long long)nb);
+    const int r = (int)((key / (unsigned long long)nb) % (unsigned long long)nc);
+    cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block at chunk row %d, batch %d", r, b + off);
+    if (err) err->chunk_index = r, err->batch_index = b + off;
+    return s;
+  }
+  for (int j = 0; j < np; ++j)
+    if (!std::isfinite(grad_out[j]))
+      return fail(err, CKO_NON_FINITE, "parameter product of the model is not finite");
+  if (loss_out) *loss_out = L;
+  if (bwd) {
+    std::memset(bwd, 0, sizeof(*bwd));
+    for (int step_hi = nt; step_hi >= 1;) {
+      const int cc = nc < step_hi ? nc : step_hi;
+      bwd->jacobian_evals += 1;
+      bwd->linear_solves += 1;
+      bwd->reduction_sweeps += sweeps_of(cc, sv->kind, sv->n_switch);
+      step_hi -= cc;
+    }
+  }
+  return ok(err);
+}
+
+}  // namespace
+
+extern "C" {
+
+cko_status cko_be_forward_device(cko_ctx* c, const cko_model* m, const double* d_y0, const double* d_times, int nb,
+                                 int nt, int nc, const cko_newton_settings* st, const cko_solver_choice* sv,
+                                 double* d_states, cko_work* work, cko_error* err) {
+  if (!c || !m || !d_y0 || !d_times || !d_states || !st || !sv) return fail(err, CKO_ERROR, "null argument");
+  if (nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: y0 rows != grid batch width");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  if (d_states != d_y0)
+    CUDA_TRY(cudaMemcpyAsync(d_states, d_y0, sizeof(double) * row, cudaMemcpyDeviceToDevice, c->stream));
+  return forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, work, nullptr, err);
+}
+
+cko_status cko_be_forward(cko_ctx* c, const cko_model* m, const double* y0, const double* times, int nb, int nt,
+                          int nc, const cko_newton_settings* st, const cko_solver_choice* sv, double* states_out,
+                          cko_traj** traj_out, cko_work* work, cko_error* err) {
+  if (!c || !m || !y0 || !times || !st || !sv) return fail(err, CKO_ERROR, "null argument");
+  if (traj_out) *traj_out = nullptr;
+  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int n = m->dm.n;
+  const size_t row = (size_t)nb * n;
+  cko_traj* t = nullptr;
+  double *d_states, *d_times;
+  if (traj_out) {
+    t = new (std::nothrow) cko_traj();
+    if (!t) return fail(err, CKO_ERROR, "out of host memory");
+    t->ctx = c;
+    t->nb = nb;
+    t->nt = nt;
+    t->n = n;
+    cudaError_t e = cudaMalloc(&t->d_states, sizeof(double) * row * (nt + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&t->d_times, sizeof(double) * (size_t)nb * (nt + 1));
+    if (e != cudaSuccess) {
+      cudaFree(t->d_states);
+      cudaFree(t->d_times);
+      delete t;
+      return fail(err, CKO_CUDA, "trajectory allocation: %s", cudaGetErrorString(e));
+    }
+    d_states = t->d_states;
+    d_times = t->d_times;
+  } else {
+    CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
+    CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
+    d_states = c->h_states.as<double>();
+    d_times = c->h_times.as<double>();
+  }
+  auto cleanup = [&](cko_status s) {
+    if (s != CKO_OK && t) {
+      cudaFree(t->d_states);
+      cudaFree(t->d_times);
+      delete t;
+      t = nullptr;
+    }
+    return s;
+  };
+  cudaError_t e = cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice,
+                                  c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) return cleanup(fail(err, CKO_CUDA, "H2D: %s", cudaGetErrorString(e)));
+  cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, work, nullptr, err);
+  if (s != CKO_OK) return cleanup(s);
+  if (states_out) {
+    e = cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cleanup(fail(err, CKO_CUDA, "D2H: %s", cudaGetErrorString(e)));
+  }
+  if (traj_out) *traj_out = t;
+  return ok(err);
+}
+
+cko_status cko_be_adjoint_device(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times,
+                                 int nb, int nt, int nc, const cko_solver_choice* sv, int loss_kind,
+                                 const double* d_dL, double* loss_out, double* grad_out, cko_work* bwd,
+                                 cko_error* err) {
+  if (!c || !m || !d_states || !d_times || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (nt < 1 || nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: empty trajectory");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, loss_kind, d_dL, loss_out, grad_out, bwd, err);
+}
+
+cko_status cko_be_adjoint(cko_ctx* c, const cko_model* m, const cko_traj* t, int nc, const cko_solver_choice* sv,
+                          int loss_kind, const double* dL_host, double* loss_out, double* grad_out, cko_work* bwd,
+                          cko_error* err) {
+  if (!c || !m || !t || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (t->n != m->dm.n) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: trajectory width != model size");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const double* d_dL = nullptr;
+  if (loss_kind == CKO_LOSS_USER) {
+    if (!dL_host) return fail(err, CKO_ERROR, "user loss needs dL");
+    const size_t bytes = sizeof(double) * (size_t)t->nb * t->n * (t->nt + 1);
+    CUDA_TRY(c->h_dL.ensure(bytes));
+    CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dL_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    d_dL = c->h_dL.as<double>();
+  }
+  return adjoint_core(c, m, t->d_states, t->d_times, t->nb, t->nt, nc, sv, loss_kind, d_dL, loss_out, grad_out,
+                      bwd, err);
+}
+
+cko_status cko_be_adjoint_host(cko_ctx* c, const cko_model* m, const double* states, const double* times, int nb,
+                               int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* dL_host,
+                               double* loss_out, double* grad_out, cko_work* bwd, cko_error* err) {
+  if (!c || !m || !states || !times || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->h_states.p, states, sizeof(double) * row * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+  const double* d_dL = nullptr;
+  if (loss_kind == CKO_LOSS_USER) {
+    if (!dL_host) return fail(err, CKO_ERROR, "user loss needs dL");
+    CUDA_TRY(c->h_dL.ensure(sizeof(double) * row * (nt + 1)));
+    CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dL_host, sizeof(double) * row * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+    d_dL = c->h_dL.as<double>();
+  }
+  return adjoint_core(c, m, c->h_states.as<double>(), c->h_times.as<double>(), nb, nt, nc, sv, loss_kind, d_dL,
+                      loss_out, grad_out, bwd, err);
+}
+
+cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0, const double* times, int nb,
+                                int nt, int nc, const cko_newton_settings* st, const cko_solver_choice* sv,
+                                double* states_out, double* loss_out, double* grad_out, cko_work* fwd, cko_work* bwd,
+                                cko_error* err) {
+  if (!c || !m || !y0 || !times || !st || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
+  double* d_states = c->h_states.as<double>();
+  double* d_times = c->h_times.as<double>();
+  CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
+  if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err)) return s;
+  if (states_out) {
+    CUDA_TRY(cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost,
+                             c->stream));
+  }
+  return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out, grad_out, bwd,
+                      err);
+}
+
+cko_status cko_traj_states(const cko_traj* t, const double** d_states, int* nb, int* nt, int* n) {
+  if (!t) return CKO_ERROR;
+  if (d_states) *d_states = t->d_states;
+  if (nb) *nb = t->nb;
+  if (nt) *nt = t->nt;
+  if (n) *n = t->n;
+  return CKO_OK;
+}
+
+cko_status cko_traj_destroy(cko_traj* t) {
+  if (!t) return CKO_OK;
+  cudaSetDevice(t->ctx->device);
+  cudaFree(t->d_states);
+  cudaFree(t->d_times);
+  delete t;
+  return CKO_OK;
+}
+
+cko_status cko_block_bidiag_solve(cko_ctx* c, const cko_solver_choice* sv, int nc, int nb, int n,
+                                  const double* diag, const double* offdiag, double* rhs, long long* sweeps,
+                                  cko_error* err) {
+  if (!c || !sv || !diag || !rhs) return fail(err, CKO_ERROR, "null argument");
+  if (nc < 1 || nb < 1 || n < 1) return fail(err, CKO_SHAPE_MISMATCH, "block bidiagonal system must be non-empty");
+  if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
+  if (sv->kind == CKO_SOLVER_HYBRID && sv->n_switch < 0)
+    return fail(err, CKO_ERROR, "solve_hybrid: n_switch must be >= 0");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t nd = (size_t)nc * nb * n * n, no = (size_t)(nc > 1 ? nc - 1 : 0) * nb * n * n,
+               nr = (size_t)nc * nb * n;
+  CUDA_TRY(c->h_diag.ensure(sizeof(double) * nd));
+  CUDA_TRY(c->h_rhs.ensure(sizeof(double) * nr));
+  CUDA_TRY(cudaMemcpyAsync(c->h_diag.p, diag, sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_rhs.p, rhs, sizeof(double) * nr, cudaMemcpyHostToDevice, c->stream));
+  const double* d_off = nullptr;
+  if (offdiag) {
+    CUDA_TRY(c->h_off.ensure(sizeof(double) * (no ? no : 1)));
+    if (no) CUDA_TRY(cudaMemcpyAsync(c->h_off.p, offdiag, sizeof(double) * no, cudaMemcpyHostToDevice, c->stream));
+    d_off = c->h_off.as<double>();
+  }
+  const int G = nb < 2 * c->sms ? nb : 2 * c->sms;
+  Slab slab;
+  if (cko_status s = prepare_slab(c, G, nb, nc, n, sv->kind != CKO_SOLVER_THOMAS || offdiag, slab, err)) return s;
+  CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+  SolveLaunch a{};
+  a.diag = c->h_diag.as<double>();
+  a.offdiag = d_off;
+  a.x = c->h_rhs.as<double>();
+  a.nc = nc;
+  a.nb = nb;
+  a.n = n;
+  a.solver = sv->kind;
+  a.n_switch = sv->n_switch;
+  a.slab = slab;
+  a.sing_key = c->key.as<unsigned long long>();
+  a.grid = G;
+  a.threads = kThreads;
+  CUDA_TRY(launch_solve(a, c->stream));
+  unsigned long long key;
+  CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(rhs, c->h_rhs.p, sizeof(double) * nr, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (key != ~0ull) {
+    const int k = (int)(key / (unsigned long long)nb), b = (int)(key % (unsigned long long)nb);
+    cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block at chunk row %d, batch %d", k, b);
+    if (err) err->chunk_index = k, err->batch_index = b;
+    return s;
+  }
+  if (sweeps) *sweeps = sweeps_of(nc, sv->kind, sv->n_switch);
+  return ok(err);
+}
+
+cko_status cko_newton_solve_chunk(cko_ctx* c, const cko_model* m, const double* y_start, double* dy,
+                                  const double* t_chunk, const double* dt_chunk, int cc, int nb,
+                                  const cko_newton_settings* st, const cko_solver_choice* sv, int chunk_start_step,
+                                  int* iterations, cko_work* work, cko_error* err) {
+  if (!c || !m || !y_start || !dy || !t_chunk || !dt_chunk || !st || !sv) return fail(err, CKO_ERROR, "null argument");
+  if (cc < 1 || nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "chunk op: empty chunk");
+  CUDA_TRY(cudaSetDevice(c->device));
+  // A one-chunk integration over a synthetic grid reproducing t_chunk/dt_chunk:
+  // times row 0 = t_0 - dt_0, row k+1 = t_chunk(k). dt is recomputed on the
+  // device as t(k) - t(k-1), so feed the exact differences through
+  // consecutive rows: t_prev(k) = t(k) - dt(k) must equal t(k-1).
+  const int n = m->dm.n;
+  std::vector<double> times((size_t)(cc + 1) * nb);
+  for (int b = 0; b < nb; ++b) {
+    times[b] = t_chunk[b] - dt_chunk[b];
+    for (int k = 0; k < cc; ++k) times[(size_t)(k + 1) * nb + b] = t_chunk[(size_t)k * nb + b];
+  }
+  for (int k = 1; k < cc; ++k)
+    for (int b = 0; b < nb; ++b)
+      if (t_chunk[(size_t)k * nb + b] - t_chunk[(size_t)(k - 1) * nb + b] != dt_chunk[(size_t)k * nb + b])
+        return fail(err, CKO_STRATEGY_UNAVAILABLE,
+                    "newton_solve_chunk: dt_chunk must equal consecutive t_chunk differences on the device path");
+  const size_t row = (size_t)nb * n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (cc + 1)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * times.size()));
+  CUDA_TRY(c->h_dL.ensure(sizeof(double) * row * cc));
+  double* d_states = c->h_states.as<double>();
+  CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times.data(), sizeof(double) * times.size(), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_states, y_start, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dy, sizeof(double) * row * cc, cudaMemcpyHostToDevice, c->stream));
+  cko_newton_settings s2 = *st;
+  cko_status s = forward_core(c, m, d_states, c->h_times.as<double>(), nb, cc, cc, &s2, sv, c->h_dL.as<double>(),
+                              work, iterations, err);
+  if (s != CKO_OK) {
+    if (s == CKO_NEWTON_DIVERGENCE && err) err->chunk_start_step = chunk_start_step;
+    return s;
+  }
+  std::vector<double> out(row * (cc + 1));
+  CUDA_TRY(cudaMemcpy(out.data(), d_states, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < cc; ++k)
+    for (size_t i = 0; i < row; ++i) dy[(size_t)k * row + i] = out[(size_t)(k + 1) * row + i] - y_start[i];
+  return ok(err);
+}
+
+}  // extern "C"

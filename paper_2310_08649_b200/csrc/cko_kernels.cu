@@ -1,0 +1,186 @@
+// cko_kernels.cu — non-template kernels (standalone solver, loss, VJP
+// reduction) and the per-model dispatch of the launch interface.
+//
+// Kernel overview (templates in cko_impl.cuh, one TU per model in cko_inst_*.cu):
+//  fwd_kernel  : the whole forward integration (integrate.cpp:321-369) in one
+//                cooperative persistent launch; CTAs own disjoint lane ranges
+//                and meet only in the all-lanes Newton predicate
+//                (integrate.cpp:176-182), one flag OR-reduction per iteration.
+//  adj_kernel  : the discrete adjoint (adjoint.cpp:49-127, 263-297), lane
+//                parallel with no grid barrier; emits w_m = lambda_m dt_m.
+//  vjp_kernel  : sum of w . dh/dp over all points (ode_model.cpp:135-153),
+//                reduced deterministically.
+#include "cko_impl.cuh"
+
+namespace cko {
+
+CKO_DECLARE(scalar)
+CKO_DECLARE(constant)
+CKO_DECLARE(lin3)
+CKO_DECLARE(mds)
+CKO_DECLARE(chaboche)
+CKO_DECLARE(node)
+
+size_t slab_doubles_per_point(int n, bool pcr) {
+  return 2 * (size_t)n + (size_t)n * n + 1 + (pcr ? 3 * (size_t)n * n + n : 0);
+}
+
+// ---------------------------------------------------------------------------
+// standalone block-bidiagonal solve
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kMaxThreads) solve_kernel(SolveLaunch a) {
+  const int nb = a.nb, n = a.n, T = blockDim.x, tid = threadIdx.x, nc = a.nc;
+  int lb0, L;
+  lane_range(nb, lb0, L);
+  const bool general = a.offdiag != nullptr;
+  CtaWs w = make_ws(a.slab, n, a.solver != 0 || general);
+  for (int p = tid; p < nc * L; p += T) {
+    const int k = p / L, lb = p % L, b = lb0 + lb;
+    SBlk A = w.b(w.lu, p);
+    const double* src = a.diag + ((size_t)k * nb + b) * n * n;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) A(i, j) = src[i * n + j];
+    SVec x = w.v(w.hr, p);
+    for (int i = 0; i < n; ++i) x[i] = a.x[((size_t)k * nb + b) * n + i];
+    if (general && k >= 1) {
+      SBlk Bm = w.b(w.B, p);
+      const double* o = a.offdiag + ((size_t)(k - 1) * nb + b) * n * n;
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) Bm(i, j) = o[i * n + j];
+    }
+    if (!lu_factor(A, w.pv(p), n)) atomicMin(a.sing_key, (unsigned long long)k * nb + b);
+  }
+  __syncthreads();
+  if (a.solver == 0) {
+    if (!general) {
+      cta_thomas_unit(w, nc, L, false);
+    } else {
+      for (int lb = tid; lb < L; lb += T)
+        for (int k = 0; k < nc; ++k) {
+          const int p = k * L + lb;
+          if (k > 0) gemv_sub_into(w.b(w.B, p), w.v(w.hr, p - L), w.v(w.hr, p), w.v(w.hr, p), n);
+          lu_solve(w.b(w.lu, p), w.pv(p), n, w.v(w.hr, p));
+        }
+    }
+  } else {
+    cta_pcr(w, nc, L, a.solver == 1 ? -1 : a.n_switch, !general);
+  }
+  __syncthreads();
+  for (int p = tid; p < nc * L; p += T) {
+    const int k = p / L, b = lb0 + p % L;
+    SVec x = w.v(w.hr, p);
+    for (int i = 0; i < n; ++i) a.x[((size_t)k * nb + b) * n + i] = x[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// loss: L = sqrt(sum_{m >= 1} y^2), two-pass deterministic reduction
+// ---------------------------------------------------------------------------
+constexpr int kLossBlocks = 1024;
+
+__device__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) s += sh[i];
+  __syncthreads();
+  return s;
+}
+
+__global__ void loss_partial_kernel(const double* states, size_t count, double* part) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  const size_t per = (count + gridDim.x - 1) / gridDim.x;
+  const size_t lo = per * blockIdx.x, hi = min(count, lo + per);
+  for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += states[i] * states[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void loss_final_kernel(const double* part, int np, double* loss) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) *loss = sqrt(s);
+}
+
+cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
+                        cudaStream_t st) {
+  const size_t count = (size_t)nt * row;
+  loss_partial_kernel<<<kLossBlocks, 256, 0, st>>>(states + row, count, scratch);
+  loss_final_kernel<<<1, 1024, 0, st>>>(scratch, kLossBlocks, loss);
+  return cudaGetLastError();
+}
+
+__global__ void vjp_final_kernel(const double* part, int nblk, int np, double* grad) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < np; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < nblk; ++q) s += part[(size_t)q * np + j];
+    grad[j] = s;
+  }
+}
+
+
+size_t vjp_scratch_doubles(const DevModel& m) { return (size_t)kVjpBlocks * m.np; }
+
+#define CKO_SWITCH(KIND, CALL)            \
+  switch (KIND) {                         \
+    case 0: return CALL(scalar);          \
+    case 1: return CALL(constant);        \
+    case 2: return CALL(lin3);            \
+    case 3: return CALL(mds);             \
+    case 4: return CALL(chaboche);        \
+    case 5: return CALL(node);            \
+  }                                       \
+  return cudaErrorInvalidValue;
+
+cudaError_t launch_forward(const FwdLaunch& a, cudaStream_t st) {
+#define CALL(N) fwd_run_##N(a, st)
+  CKO_SWITCH(a.m.kind, CALL)
+#undef CALL
+}
+
+static cudaError_t occ(int kind, int threads, int* blocks) {
+#define CALL(N) fwd_occ_##N(threads, blocks)
+  CKO_SWITCH(kind, CALL)
+#undef CALL
+}
+
+int forward_max_grid(int kind, int threads, int device) {
+  int blocks = 0, sms = 0;
+  if (occ(kind, threads, &blocks) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return blocks * sms;
+}
+
+cudaError_t launch_adjoint(const AdjLaunch& a, cudaStream_t st) {
+#define CALL(N) adj_run_##N(a, st)
+  CKO_SWITCH(a.m.kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st) {
+  solve_kernel<<<a.grid, a.threads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+static cudaError_t vjp_dispatch(const DevModel& m, const double* states, const double* times, const double* wq,
+                                int nb, int nt, double* scratch, cudaStream_t st) {
+#define CALL(N) vjp_run_##N(m, states, times, wq, nb, nt, scratch, st)
+  CKO_SWITCH(m.kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
+                       int nt, double* scratch, double* grad, cudaStream_t st) {
+  cudaError_t e = vjp_dispatch(m, states, times, wq, nb, nt, scratch, st);
+  if (e != cudaSuccess) return e;
+  vjp_final_kernel<<<(m.np + 255) / 256, 256, 0, st>>>(scratch, kVjpBlocks, m.np, grad);
+  return cudaGetLastError();
+}
+
+}  // namespace cko

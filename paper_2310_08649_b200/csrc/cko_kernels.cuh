@@ -1,0 +1,90 @@
+// cko_kernels.cuh — launch interface between the C ABI (cko_api.cu) and the
+// sm_100a kernels (cko_kernels.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "cko_common.cuh"
+#include "cko_models.cuh"
+
+namespace cko {
+
+// Per-CTA workspace slab. Arrays are [elements][Pmax] with Pmax = nc * Lmax
+// points (point p = row * L + local lane).
+struct Slab {
+  double* base;    // G slabs of `doubles` each
+  int* pbase;      // G pivot slabs of `ints` each
+  size_t doubles;  // per CTA
+  size_t ints;     // per CTA
+  int Pmax;
+  int Lmax;
+};
+
+size_t slab_doubles_per_point(int n, bool pcr);
+
+struct FwdLaunch {
+  DevModel m;
+  double* states;        // (nt+1, nb, n), row 0 = y0 on entry
+  const double* times;   // (nt+1, nb)
+  const double* dy_init; // optional (nc, nb, n): initial increments (newton_solve_chunk)
+  int nb, nt, nc;
+  double tol_a, tol_r;
+  int max_iter;
+  int solver, n_switch;
+  Slab slab;
+  double* rn;             // (nb) last residual norms
+  double* r0;             // (nb) initial residual norms of the current chunk
+  int* iters;             // (n_chunks) Newton iterations per chunk
+  GridSync* gs;
+  GroupView grp;
+  unsigned long long* sing_key;  // min over k * nb + b of singular blocks
+  int* info;             // [0] status, [1] chunk_start_step, [2] iterations, [3] n_chunks done
+  uint64_t budget_ns;
+  int grid;               // CTAs
+  int threads;
+};
+
+struct AdjLaunch {
+  DevModel m;
+  const double* states;  // (nt+1, nb, n)
+  const double* times;   // (nt+1, nb)
+  const double* dL;      // optional user dL (nt+1, nb, n); null = Frobenius y / L
+  const double* loss;    // device scalar L (Frobenius)
+  int nb, nt, nc;
+  int solver, n_switch;
+  Slab slab;
+  double* lambda;        // (nb, n)
+  double* wq;            // (nt+1, nb, n) quadrature weights lambda_m dt_m (row 0 unused)
+  unsigned long long* sing_key;  // min over (chunk ordinal, r, b)
+  int grid;
+  int threads;
+};
+
+struct SolveLaunch {
+  const double* diag;     // (nc, nb, n, n)
+  const double* offdiag;  // (nc-1, nb, n, n) or null (-I)
+  double* x;              // (nc, nb, n) rhs in, solution out
+  int nc, nb, n;
+  int solver, n_switch;
+  Slab slab;
+  unsigned long long* sing_key;
+  int grid;
+  int threads;
+};
+
+cudaError_t launch_forward(const FwdLaunch& a, cudaStream_t st);
+int forward_max_grid(int kind, int threads, int device);
+cudaError_t launch_adjoint(const AdjLaunch& a, cudaStream_t st);
+cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st);
+// L = sqrt(sum_{m>=1} y^2) into *loss (device); scratch >= 1024 doubles.
+cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
+                        cudaStream_t st);
+// grad (device, np) = sum over (m >= 1, b) of w . dh/dp; scratch sized by vjp_scratch_doubles.
+size_t vjp_scratch_doubles(const DevModel& m);
+cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times,
+                       const double* wq, int nb, int nt, double* scratch, double* grad,
+                       cudaStream_t st);
+
+}  // namespace cko
