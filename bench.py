@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""Benchmark: series*steps/s of backward-Euler forward + discrete adjoint (PCR).
+
+Workload (BASELINE.json configs[1]): mass-damper-spring chain,
+10 units (n = 20), nb = 1000 series per GPU, nt = 10000 steps, t_max = 0.01
+(finite horizon), y0 = 0, Frobenius loss, analytic Jacobians,
+PCR block-bidiagonal solves at n_chunk = --n-chunk. Synthetic inputs (the
+reference's own deterministic model parameters and uniform time grid).
+
+One step = integrate_backward_euler + adjoint_backward over the whole
+workload, inputs resident in HBM (value) / through the C ABI from pinned host
+buffers (e2e). Inputs (1.6 GB trajectory, 80 MB grid) exceed the 126 MB L2,
+so no explicit flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Under torchrun each rank integrates its own nb lanes of a global
+nb * world-lane problem (weak scaling, lane_offset sharding); the only
+cross-rank traffic is the per-Newton-iteration convergence flag and the
+loss / gradient sums.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nb", type=int, default=1000, help="series per GPU")
+    ap.add_argument("--nt", type=int, default=10000)
+    ap.add_argument("--n-unit", type=int, default=10)
+    ap.add_argument("--t-max", type=float, default=0.01)
+    ap.add_argument("--n-chunk", type=int, default=16)
+    ap.add_argument("--solver", default="pcr", choices=["thomas", "pcr", "hybrid"])
+    ap.add_argument("--n-switch", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=32)
+    ap.add_argument("--quiet-clocks", action="store_true", help="skip nvidia-smi sampling (profiler runs)")
+    return ap.parse_args()
+
+
+SOLVER_ID = {"thomas": 0, "pcr": 1, "hybrid": 2}
+
+
+def uniform_times(nt, nb, t_max):
+    ti = np.array([t_max * float(i) / float(nt) for i in range(nt + 1)])
+    return np.ascontiguousarray(np.repeat(ti[:, None], nb, axis=1))
+
+
+def sweeps_per_solve(c, solver, n_switch):
+    if solver == "thomas":
+        return 0
+    s = 0
+    for bit in range(30, -1, -1):
+        m = 1 << bit
+        if c & m:
+            e = m.bit_length() - 1
+            s += e if solver == "pcr" else min(n_switch, e)
+    return s
+
+
+def flops_per_series_step(n, nc, solver, n_switch, k_avg):
+    """Algorithmic fp64 flops per series*step (MDS analytic model):
+    forward: (k+1) residual passes (rate ~ 8u + 3n each) + k x [J assembly n^2,
+    LU L(n), solve 2n^2 (+ PCR sweeps)], adjoint: one J^T lambda (2n^2), one LU,
+    one solve (+ sweeps), quadrature + VJP (~12u). PCR adds (4n^3 + 2n^2) per
+    row per sweep beyond the first-level right solve, averaged over the chunk."""
+    L = sum(1 + m + 2 * m * m for m in range(n))
+    u = n // 2
+    F_h = 8 * u + 3 * n
+    sw = sweeps_per_solve(nc, solver, n_switch) / max(nc, 1)  # sweeps per row
+    pcr_row = sw * (4 * n ** 3 + 2 * n * n) if solver != "thomas" else 0.0
+    fwd = (k_avg + 1) * F_h + k_avg * (n * n + L + 2 * n * n + pcr_row)
+    adj = 2 * n * n + n * n + L + 2 * n * n + pcr_row + 12 * u + 2 * n
+    return fwd + adj
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device, enabled=True):
+        self.device, self.enabled, self.proc, self.lines = device, enabled, None, []
+
+    def __enter__(self):
+        if self.enabled:
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                time.sleep(0.3)
+            except OSError:
+                self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def mds_workload(args, world, rank):
+    import paper_2310_08649_b200 as P
+    nb_total = args.nb * world
+    model = P.build_mass_damper_spring(args.n_unit, nb_total)
+    times = uniform_times(args.nt, args.nb, args.t_max)
+    y0 = np.zeros((args.nb, model.state_size))
+    return model.shard(rank * args.nb), y0, times
+
+
+def config_dict(args, world, extra=None):
+    d = {"workload": (f"C2 mass-damper-spring chain (SURVEY §8d): {args.n_unit} units (n={2 * args.n_unit}), "
+                      f"nb={args.nb}/GPU, nt={args.nt}, t_max={args.t_max}, backward Euler + discrete adjoint, "
+                      f"{args.solver} n_chunk={args.n_chunk}, Frobenius loss"),
+         "model": "mds", "n_unit": args.n_unit, "n_size": 2 * args.n_unit, "n_batch_per_gpu": args.nb,
+         "n_batch_total": args.nb * world, "n_time": args.nt, "n_chunk": args.n_chunk, "solver": args.solver,
+         "t_max": args.t_max, "parallelism": f"batch-sharded dp{world}",
+         "l2": "inputs larger than L2 (trajectory 1.6 GB/GPU, grid 80 MB), no flush"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the compiled reference (oracle/_ref) on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import load_port, load_ref, ref_available
+    kind = "reference" if ref_available() else "port"
+    orc = load_ref() if kind == "reference" else load_port()
+    cores = os.cpu_count() or 1
+    nt_s = args.cpu_sample_steps
+    model, y0, _ = mds_workload(args, 1, 0)
+    times = uniform_times(nt_s, args.nb, args.t_max * nt_s / args.nt)  # same dt as the full grid
+    nc = min(args.n_chunk, nt_s)
+    sv = (SOLVER_ID[args.solver], args.n_switch)
+    secs = []
+    for i in range(args.warmup + args.steps):
+        s = orc.sharded_seconds(model, y0, times, nc, cores, solver=sv)
+        if s < 0:
+            raise SystemExit("reference run failed")
+        if i >= args.warmup:
+            secs.append(s)
+    sec = statistics.mean(secs)
+    v = args.nb * nt_s / sec
+    line = {"impl": "reference", "metric": "series*steps/s forward+adjoint (backward Euler, PCR)",
+            "value": v, "unit": "series*steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, 1, {"sample": f"nb={args.nb} x nt={nt_s} steps (dt as full grid)"}),
+            "cpu_baseline": {"value": v, "unit": "series*steps/s", "cores": cores, "kind": kind,
+                             "sample": f"nb={args.nb} lanes x {nt_s} steps per step, {cores} threads over "
+                                       f"contiguous lane shards (timing only: shard-local Newton predicate)"},
+            "e2e": {"value": v, "unit": "series*steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_single(args):
+    """Single-thread compiled reference on a bounded sample (rank 0, N = 1)."""
+    from oracle import load_port, load_ref, ref_available
+    kind = "reference" if ref_available() else "port"
+    orc = load_ref() if kind == "reference" else load_port()
+    nt_s = args.cpu_sample_steps
+    model, y0, _ = mds_workload(args, 1, 0)
+    times = uniform_times(nt_s, args.nb, args.t_max * nt_s / args.nt)
+    nc = min(args.n_chunk, nt_s)
+    t0 = time.perf_counter()
+    orc.gradient(model, y0, times, nc, solver=(SOLVER_ID[args.solver], args.n_switch))
+    sec = time.perf_counter() - t0
+    return {"value": args.nb * nt_s / sec, "unit": "series*steps/s", "cores": 1, "kind": kind,
+            "sample": f"nb={args.nb} lanes x first {nt_s} steps (same dt), single thread, forward+adjoint, "
+                      f"{sec:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_08649_b200 import abi, api
+    from paper_2310_08649_b200._native import lib
+    from paper_2310_08649_b200.errors import raise_for
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    model, y0, times = mds_workload(args, world, rank)
+    nb, nt, n = args.nb, args.nt, model.state_size
+    ctx = api.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    if world > 1:
+        from paper_2310_08649_b200 import group
+        group.join(ctx, rank, world)
+    L = lib()
+    dm = ctx.model(model)
+    d_y0 = torch.from_numpy(y0).cuda()
+    d_times = torch.from_numpy(times).cuda()
+    d_states = torch.empty((nt + 1, nb * n), dtype=torch.float64, device="cuda")
+    st = api.NewtonSettings().c()
+    sv = api.SolverChoice(SOLVER_ID[args.solver], args.n_switch).c()
+    grad = np.zeros(model.params.size)
+    loss = C.c_double()
+    wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+    L.cko_ctx_enable_timing(ctx.h, 1)
+    kms = (C.c_double * 4)()
+
+    def step(record=None):
+        rc = L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()), nb, nt,
+                                     args.n_chunk, C.byref(st), C.byref(sv), C.c_void_p(d_states.data_ptr()),
+                                     C.byref(wf), C.byref(e))
+        raise_for(rc, e)
+        if record is not None:
+            L.cko_ctx_last_kernel_ms(ctx.h, kms)
+            record["fwd"] += kms[0]
+            launches = L.cko_ctx_last_launches(ctx.h)
+        rc = L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()), C.c_void_p(d_times.data_ptr()),
+                                     nb, nt, args.n_chunk, C.byref(sv), abi.CKO_LOSS_FROBENIUS, None, C.byref(loss),
+                                     abi.dptr(grad), C.byref(wb), C.byref(e))
+        raise_for(rc, e)
+        if record is not None:
+            L.cko_ctx_last_kernel_ms(ctx.h, kms)
+            record["adj"] += kms[1]
+            record["vjp"] += kms[2]
+            record["loss"] += kms[3]
+            record["launches"] += launches + L.cko_ctx_last_launches(ctx.h)
+
+    for _ in range(args.warmup):
+        step()
+    rec = {"fwd": 0.0, "adj": 0.0, "vjp": 0.0, "loss": 0.0, "launches": 0}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local, enabled=not args.quiet_clocks) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(rec)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = nb * world * nt / (ms * 1e-3)
+
+    # ---- e2e: the public C ABI with pinned HOST buffers, H2D/D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        h_y0 = torch.from_numpy(y0).pin_memory()
+        h_times = torch.from_numpy(times).pin_memory()
+        hp = lambda t: C.cast(C.c_void_p(t.data_ptr()), C.POINTER(C.c_double))  # noqa: E731
+        L.cko_ctx_enable_timing(ctx.h, 0)
+
+        def e2e_step():
+            rc = L.cko_gradient_adjoint(ctx.h, dm, hp(h_y0), hp(h_times), nb, nt, args.n_chunk, C.byref(st),
+                                        C.byref(sv), None, C.byref(loss), abi.dptr(grad), C.byref(wf), C.byref(wb),
+                                        C.byref(e))
+            raise_for(rc, e)
+        for _ in range(2):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": nb * world * nt / (e_ms * 1e-3), "unit": "series*steps/s",
+               "h2d_bytes_per_step": int(h_y0.numel() * 8 + h_times.numel() * 8),
+               "d2h_bytes_per_step": int(grad.size * 8 + 8), "ms_per_step": e_ms,
+               "path": "cko_gradient_adjoint (C ABI, pinned host y0/times -> loss + gradient)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    k = args.steps
+    kern = {"fwd_kernel": rec["fwd"] / k, "adj_kernel": rec["adj"] / k, "vjp_kernels": rec["vjp"] / k,
+            "loss_kernels": rec["loss"] / k}
+    dom = max(kern, key=kern.get)
+    hbm_peak = 6536.7
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        peak_src = "fallback"
+    units = nb * nt  # series*steps per launch on this rank
+    bytes_per = {"fwd_kernel": 8 * n + 8, "adj_kernel": 8 * n + 8 + 8 * n, "vjp_kernels": 8 * n + 8 + 8 * n,
+                 "loss_kernels": 8 * n}[dom]
+    achieved = units * bytes_per / (kern[dom] * 1e-3) / 1e9
+    k_avg = wf.newton_iterations / max(1, math.ceil(nt / args.n_chunk))
+    fl = flops_per_series_step(n, args.n_chunk, args.solver, args.n_switch, k_avg)
+    tf = C.c_double(0.0)
+    L.cko_probe_fp64_tflops(ctx.h, C.byref(tf), C.byref(e))
+    step_tflops = units * fl / (ms * 1e-3) / 1e12
+    line = {
+        "metric": "series*steps/s forward+adjoint (backward Euler, PCR)",
+        "value": value, "unit": "series*steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference model parameters, uniform grid, y0 = 0)",
+        "config": config_dict(args, world),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_src,
+                     "alg_bytes_per_series_step": bytes_per, "kernel_ms": kern[dom]},
+        "roofline_fp64": {"bound": "fp64", "achieved": step_tflops, "peak": tf.value, "unit": "TFLOP/s",
+                          "frac": step_tflops / tf.value if tf.value else None,
+                          "peak_source": "measured DFMA probe (cko_probe_fp64_tflops)",
+                          "alg_flops_per_series_step": fl, "note": "whole step (fwd+adj), all kernels"},
+        "kernel_ms_per_step": kern,
+        "newton": {"fwd": {kk: int(getattr(wf, kk)) for kk, _ in abi.CkoWork._fields_},
+                   "bwd": {kk: int(getattr(wb, kk)) for kk, _ in abi.CkoWork._fields_}},
+        "loss": loss.value,
+        "gpu_launches": rec["launches"],
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_single(args)
+        except Exception as ex:  # the checker build is missing on this box
+            line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    line["clocks"] = clk.summary()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

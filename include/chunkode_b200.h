@@ -133,12 +133,20 @@ cko_status cko_ctx_destroy(cko_ctx* ctx);
 /* Use an external stream (cudaStream_t) instead of the context's own. */
 cko_status cko_ctx_set_stream(cko_ctx* ctx, void* cuda_stream);
 /* Batch sharding: join a group of `world` ranks, one per GPU.
- * `peer_flags` are this rank's view of every rank's exchange buffer (device
- * pointers made accessible through CUDA IPC/P2P by the caller, world entries,
- * each >= cko_comm_buffer_bytes()). With world == 1 sharding is off. */
+ * `peer_buffers` are this rank's view of every rank's exchange buffer (device
+ * pointers made accessible through CUDA IPC/P2P, world entries, each
+ * cko_comm_buffer_bytes() long, own buffer at index rank). The forward kernel
+ * then ORs its Newton predicate flags across ranks every iteration, and the
+ * adjoint sums the loss and the gradient across ranks, all through P2P stores
+ * over NVLink. With world == 1 sharding is off. */
 size_t cko_comm_buffer_bytes(void);
 cko_status cko_ctx_set_group(cko_ctx* ctx, int rank, int world, void* const* peer_buffers,
                              cko_error* err);
+/* Allocate this rank's zeroed exchange buffer and export its CUDA IPC handle
+ * (64 bytes) for the peers; open a peer's handle into this process. The
+ * caller moves handles between ranks (e.g. torch.distributed all_gather). */
+cko_status cko_comm_alloc(cko_ctx* ctx, void** dev_buf, void* ipc_handle_out, cko_error* err);
+cko_status cko_comm_open(cko_ctx* ctx, const void* ipc_handle, void** peer_buf, cko_error* err);
 
 /* ---- models ------------------------------------------------------------- */
 /* Validate `desc` and upload its parameters to the device once.
@@ -225,6 +233,19 @@ cko_status cko_newton_solve_chunk(cko_ctx* ctx, const cko_model* model, const do
                                   int c, int nb, const cko_newton_settings* settings,
                                   const cko_solver_choice* solver, int chunk_start_step,
                                   int* iterations, cko_work* work, cko_error* err);
+
+/* ---- measurement ----------------------------------------------------------- */
+/* Record CUDA events around every kernel launch on the context stream;
+ * cko_ctx_last_kernel_ms returns the durations of the last call's kernels:
+ * out[0] forward kernel, out[1] adjoint kernel, out[2] parameter-VJP
+ * kernels, out[3] loss kernels (0 when not launched). */
+cko_status cko_ctx_enable_timing(cko_ctx* ctx, int on);
+cko_status cko_ctx_last_kernel_ms(cko_ctx* ctx, double* out4);
+/* Kernel launches made by the last forward / adjoint call (for accounting). */
+int cko_ctx_last_launches(cko_ctx* ctx);
+/* FP64 FMA-pipe throughput probe (dependent-chain-free DFMA stream over all
+ * SMs); writes TFLOP/s (2 flops per DFMA). The FP64 roof for the roofline. */
+cko_status cko_probe_fp64_tflops(cko_ctx* ctx, double* tflops, cko_error* err);
 
 #ifdef __cplusplus
 }

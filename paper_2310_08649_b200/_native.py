@@ -56,6 +56,12 @@ def lib() -> C.CDLL:
         "cko_traj_states": ([vp, P(vp), P(C.c_int), P(C.c_int), P(C.c_int)], C.c_int),
         "cko_traj_destroy": ([vp], C.c_int),
         "cko_block_bidiag_solve": ([vp, P(S), C.c_int, C.c_int, C.c_int, dp, dp, dp, P(C.c_longlong), P(E)], C.c_int),
+        "cko_comm_alloc": ([vp, P(vp), C.c_char_p, P(E)], C.c_int),
+        "cko_comm_open": ([vp, C.c_char_p, P(vp), P(E)], C.c_int),
+        "cko_ctx_enable_timing": ([vp, C.c_int], C.c_int),
+        "cko_ctx_last_kernel_ms": ([vp, dp], C.c_int),
+        "cko_ctx_last_launches": ([vp], C.c_int),
+        "cko_probe_fp64_tflops": ([vp, dp, P(E)], C.c_int),
         "cko_newton_solve_chunk": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, P(N), P(S), C.c_int, P(C.c_int), P(W),
                                     P(E)], C.c_int),
     }
@@ -75,5 +81,6 @@ EXPORTS = [
     "cko_ctx_set_stream", "cko_comm_buffer_bytes", "cko_ctx_set_group", "cko_model_create", "cko_model_destroy",
     "cko_be_forward", "cko_be_forward_device", "cko_be_adjoint", "cko_be_adjoint_host", "cko_be_adjoint_device",
     "cko_gradient_adjoint", "cko_traj_states", "cko_traj_destroy", "cko_block_bidiag_solve",
-    "cko_newton_solve_chunk",
+    "cko_newton_solve_chunk", "cko_ctx_enable_timing", "cko_ctx_last_kernel_ms", "cko_ctx_last_launches",
+    "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open",
 ]

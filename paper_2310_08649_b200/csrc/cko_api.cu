@@ -7,6 +7,7 @@
 // cko_kernels.cu and maps device status words back to the reference error
 // types (errors.hpp:9-69). No CPU fallback exists: without a usable CUDA
 // device every entry point returns CKO_CUDA.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -126,11 +127,26 @@ struct cko_ctx {
   bool own_stream = false;
   int sms = 0;
   // workspace pool
-  Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad;
+  Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
   Buf h_y0, h_times, h_states, h_dL, h_rhs, h_diag, h_off;  // staging for host-buffer calls
   std::vector<int> iters_host;
   // batch sharding
   GroupView grp{};
+  // kernel timing (cko_ctx_enable_timing)
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  double last_ms[4] = {0, 0, 0, 0};
+  int last_launches = 0;
+  void mark(int i) {
+    if (timing) cudaEventRecord(ev[i], stream);
+  }
+  void collect(int first_pair, int npairs) {
+    if (!timing) return;
+    for (int k = first_pair; k < first_pair + npairs; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]) == cudaSuccess) last_ms[k] = ms;
+    }
+  }
 };
 
 struct cko_model {
@@ -153,7 +169,9 @@ extern "C" {
 int cko_abi_version(void) { return CKO_ABI_VERSION; }
 int cko_model_state_size(const cko_model_desc* d) { return d ? state_size(d) : -1; }
 int cko_model_param_count(const cko_model_desc* d) { return d ? param_count(d) : -1; }
-size_t cko_comm_buffer_bytes(void) { return sizeof(unsigned long long) * 2 * 8; }
+constexpr int kRedCap = 32768;  // doubles per rank row of the peer reduce buffer
+constexpr size_t kSlotBytes = 256;
+size_t cko_comm_buffer_bytes(void) { return kSlotBytes + sizeof(double) * 2 * 8 * (size_t)kRedCap; }
 
 cko_status cko_ctx_create(int device, cko_ctx** out, cko_error* err) {
   if (!out) return fail(err, CKO_ERROR, "cko_ctx_create: null output");
@@ -191,13 +209,58 @@ cko_status cko_ctx_destroy(cko_ctx* c) {
   if (!c) return CKO_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (Buf* b : {&c->slab, &c->piv, &c->rn, &c->r0, &c->iters, &c->gs, &c->key, &c->info, &c->loss,
+  for (Buf* b : {&c->slab, &c->piv, &c->rn, &c->r0, &c->iters, &c->gs, &c->key, &c->info, &c->loss, &c->status,
                  &c->scratch, &c->lambda, &c->wq, &c->vjp, &c->grad, &c->h_y0, &c->h_times,
                  &c->h_states, &c->h_dL, &c->h_rhs, &c->h_diag, &c->h_off})
     b->release();
+  for (cudaEvent_t& e : c->ev)
+    if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return CKO_OK;
+}
+
+cko_status cko_ctx_enable_timing(cko_ctx* c, int on) {
+  if (!c) return CKO_ERROR;
+  cudaSetDevice(c->device);
+  if (on && !c->ev[0])
+    for (cudaEvent_t& e : c->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) return CKO_CUDA;
+  c->timing = on != 0;
+  return CKO_OK;
+}
+
+cko_status cko_ctx_last_kernel_ms(cko_ctx* c, double* out4) {
+  if (!c || !out4) return CKO_ERROR;
+  for (int i = 0; i < 4; ++i) out4[i] = c->last_ms[i];
+  return CKO_OK;
+}
+
+int cko_ctx_last_launches(cko_ctx* c) { return c ? c->last_launches : 0; }
+
+cko_status cko_probe_fp64_tflops(cko_ctx* c, double* tflops, cko_error* err) {
+  if (!c || !tflops) return fail(err, CKO_ERROR, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(c->scratch.ensure(sizeof(double) * 1024));
+  cudaEvent_t a, b;
+  CUDA_TRY(cudaEventCreate(&a));
+  CUDA_TRY(cudaEventCreate(&b));
+  const int blocks = c->sms * 8, iters = 1 << 14;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    CUDA_TRY(cudaEventRecord(a, c->stream));
+    CUDA_TRY(launch_fp64_probe(c->scratch.as<double>(), blocks, iters, c->stream));
+    CUDA_TRY(cudaEventRecord(b, c->stream));
+    CUDA_TRY(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+    const double flops = 2.0 * 8.0 * iters * 256.0 * blocks;
+    if (rep > 0 && ms > 0.f) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *tflops = best;
+  return ok(err);
 }
 
 cko_status cko_ctx_set_stream(cko_ctx* c, void* s) {
@@ -214,8 +277,35 @@ cko_status cko_ctx_set_group(cko_ctx* c, int rank, int world, void* const* peers
     return fail(err, CKO_ERROR, "cko_ctx_set_group: need 1 <= world <= 8, 0 <= rank < world");
   c->grp.rank = rank;
   c->grp.world = world;
-  for (int r = 0; r < 8; ++r)
-    c->grp.peer_slots[r] = (world > 1 && r < world) ? static_cast<unsigned long long*>(peers[r]) : nullptr;
+  c->grp.red_cap = kRedCap;
+  for (int r = 0; r < 8; ++r) {
+    char* base = (world > 1 && r < world) ? static_cast<char*>(peers[r]) : nullptr;
+    c->grp.peer_slots[r] = reinterpret_cast<unsigned long long*>(base);
+    c->grp.peer_red[r] = base ? reinterpret_cast<double*>(base + kSlotBytes) : nullptr;
+  }
+  return ok(err);
+}
+
+cko_status cko_comm_alloc(cko_ctx* c, void** dev_buf, void* ipc_handle_out, cko_error* err) {
+  if (!c || !dev_buf || !ipc_handle_out) return fail(err, CKO_ERROR, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bytes = cko_comm_buffer_bytes();
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, bytes));
+  CUDA_TRY(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p));
+  std::memcpy(ipc_handle_out, &h, sizeof h);
+  *dev_buf = p;
+  return ok(err);
+}
+
+cko_status cko_comm_open(cko_ctx* c, const void* ipc_handle, void** peer_buf, cko_error* err) {
+  if (!c || !ipc_handle || !peer_buf) return fail(err, CKO_ERROR, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof h);
+  CUDA_TRY(cudaIpcOpenMemHandle(peer_buf, h, cudaIpcMemLazyEnablePeerAccess));
   return ok(err);
 }
 
@@ -365,7 +455,10 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.budget_ns = 60ull * 1000 * 1000 * 1000;
   a.grid = G;
   a.threads = kThreads;
+  c->mark(0);
   CUDA_TRY(launch_forward(a, c->stream));
+  c->mark(1);
+  c->last_launches = 1;
   int info[4];
   unsigned long long key;
   CUDA_TRY(cudaMemcpyAsync(info, c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
@@ -374,6 +467,8 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   CUDA_TRY(cudaMemcpyAsync(c->iters_host.data(), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->last_ms[1] = c->last_ms[2] = c->last_ms[3] = 0.0;
+  c->collect(0, 1);
   const int off = m->desc.lane_offset;
   if (info[0] == 4) return fail(err, CKO_COMM, "grid barrier timed out (device or peer stalled)");
   if (info[0] == 1) {
@@ -445,12 +540,22 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(c->wq.ensure(sizeof(double) * row * (nt + 1)));
   CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
   CUDA_TRY(c->loss.ensure(sizeof(double)));
-  CUDA_TRY(c->scratch.ensure(sizeof(double) * 1024));
+  CUDA_TRY(c->scratch.ensure(sizeof(double) * 1040));
+  CUDA_TRY(c->status.ensure(sizeof(unsigned)));
+  CUDA_TRY(cudaMemsetAsync(c->status.p, 0, sizeof(unsigned), c->stream));
+  if (c->grp.world > 1 && np > c->grp.red_cap)
+    return fail(err, CKO_COMM, "parameter count %d exceeds the group reduce buffer (%d)", np, c->grp.red_cap);
   CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm)));
   CUDA_TRY(c->grad.ensure(sizeof(double) * np));
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
-  if (loss_kind == CKO_LOSS_FROBENIUS)
-    CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->stream));
+  c->last_launches = 3;
+  c->mark(6);
+  if (loss_kind == CKO_LOSS_FROBENIUS) {
+    CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
+                         c->gs.as<GridSync>(), c->status.as<unsigned>(), c->stream));
+    c->last_launches += 2;
+  }
+  c->mark(7);
   AdjLaunch a{};
   a.m = m->dm;
   a.states = d_states;
@@ -468,16 +573,30 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.sing_key = c->key.as<unsigned long long>();
   a.grid = G;
   a.threads = kThreads;
+  c->mark(2);
   CUDA_TRY(launch_adjoint(a, c->stream));
+  c->mark(3);
+  c->mark(4);
   CUDA_TRY(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),
                       c->grad.as<double>(), c->stream));
+  if (c->grp.world > 1) {
+    CUDA_TRY(launch_group_sum(c->grp, c->gs.as<GridSync>(), c->grad.as<double>(), np, c->status.as<unsigned>(),
+                              c->stream));
+    c->last_launches += 1;
+  }
+  c->mark(5);
   unsigned long long key;
+  unsigned gstatus = 0;
   double L = NAN;
+  CUDA_TRY(cudaMemcpyAsync(&gstatus, c->status.p, sizeof gstatus, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
   if (loss_kind == CKO_LOSS_FROBENIUS)
     CUDA_TRY(cudaMemcpyAsync(&L, c->loss.p, sizeof L, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(grad_out, c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->last_ms[0] = 0.0;
+  c->collect(1, 3);
+  if (gstatus) return fail(err, CKO_COMM, "group reduction timed out (peer stalled)");
   const int off = m->desc.lane_offset;
   if (key != ~0ull) {
     const int b = (int)(key % (unsigned long long)nb);

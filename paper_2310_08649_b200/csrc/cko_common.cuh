@@ -71,6 +71,8 @@ struct GroupView {
   int rank;
   int world;
   unsigned long long* peer_slots[8];  // peer_slots[r] -> rank r's slot array [2][world]
+  double* peer_red[8];                // peer_red[r]   -> rank r's reduce buffer [2][world][red_cap]
+  int red_cap;
 };
 
 // Publish this rank's OR-reduced flags for generation `gen` to every peer and
@@ -148,6 +150,44 @@ __device__ inline unsigned grid_reduce_or(GridSync* gs, const GroupView& grp, un
   }
   __syncthreads();
   return *s_bcast;
+}
+
+// Deterministic sum over ranks of a small device vector (loss sum of squares,
+// parameter gradient): every rank stores its vector into row `rank` of every
+// peer's reduce buffer over NVLink (P2P stores), publishes a generation flag,
+// waits for all peers, then sums rows 0..world-1 in rank order, so all ranks
+// hold bitwise-identical results. Single block; `gs` carries the generation.
+__device__ inline void group_sum_block(const GroupView& g, GridSync* gs, const double* local, int cnt, double* out,
+                                       uint64_t budget_ns, unsigned* status) {
+  __shared__ unsigned long long s_gen;
+  __shared__ unsigned s_ok;
+  if (threadIdx.x == 0) s_gen = gs->ext_gen + 1;
+  __syncthreads();
+  const unsigned long long gen = s_gen;
+  const size_t half = (size_t)(gen & 1ull) * g.world * g.red_cap;
+  for (int r = 0; r < g.world; ++r) {
+    double* dst = g.peer_red[r] + half + (size_t)g.rank * g.red_cap;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = local[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gs->ext_gen = gen;
+    const unsigned f = group_exchange(g, gen, 0u, globaltimer_ns() + budget_ns);
+    s_ok = (f & FLAG_TIMEOUT) ? 0u : 1u;
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (threadIdx.x == 0) *status = FLAG_TIMEOUT;
+    return;
+  }
+  const double* mine = g.peer_red[g.rank] + half;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < g.world; ++r) s += ((volatile const double*)mine)[(size_t)r * g.red_cap + i];
+    out[i] = s;
+  }
 }
 
 }  // namespace cko

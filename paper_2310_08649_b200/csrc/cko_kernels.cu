@@ -100,19 +100,34 @@ __global__ void loss_partial_kernel(const double* states, size_t count, double* 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void loss_final_kernel(const double* part, int np, double* loss) {
+__global__ void loss_final_kernel(const double* part, int np, double* sumsq, double* loss, GroupView g,
+                                  GridSync* gs, uint64_t budget_ns, unsigned* status) {
   __shared__ double sh[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
   s = block_sum(s, sh);
-  if (threadIdx.x == 0) *loss = sqrt(s);
+  if (threadIdx.x == 0) sumsq[0] = s;
+  __syncthreads();
+  if (g.world > 1) group_sum_block(g, gs, sumsq, 1, sumsq, budget_ns, status);
+  __syncthreads();
+  if (threadIdx.x == 0) *loss = sqrt(sumsq[0]);
 }
 
-cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
-                        cudaStream_t st) {
+cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss, const GroupView& g,
+                        GridSync* gs, unsigned* status, cudaStream_t st) {
   const size_t count = (size_t)nt * row;
   loss_partial_kernel<<<kLossBlocks, 256, 0, st>>>(states + row, count, scratch);
-  loss_final_kernel<<<1, 1024, 0, st>>>(scratch, kLossBlocks, loss);
+  loss_final_kernel<<<1, 256, 0, st>>>(scratch, kLossBlocks, scratch + kLossBlocks, loss, g, gs,
+                                       60ull * 1000 * 1000 * 1000, status);
+  return cudaGetLastError();
+}
+
+__global__ void group_sum_kernel(GroupView g, GridSync* gs, double* v, int cnt, uint64_t budget_ns, unsigned* status) {
+  group_sum_block(g, gs, v, cnt, v, budget_ns, status);
+}
+
+cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cnt, unsigned* status, cudaStream_t st) {
+  group_sum_kernel<<<1, 256, 0, st>>>(g, gs, v, cnt, 60ull * 1000 * 1000 * 1000, status);
   return cudaGetLastError();
 }
 
@@ -180,6 +195,27 @@ cudaError_t launch_vjp(const DevModel& m, const double* states, const double* ti
   cudaError_t e = vjp_dispatch(m, states, times, wq, nb, nt, scratch, st);
   if (e != cudaSuccess) return e;
   vjp_final_kernel<<<(m.np + 255) / 256, 256, 0, st>>>(scratch, kVjpBlocks, m.np, grad);
+  return cudaGetLastError();
+}
+
+// FP64 pipe probe: 8 independent DFMA chains per thread, no memory traffic.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters) {
+  double a[8];
+  const double b = 1.0000000001, c = 1e-12;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-6 * (threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+cudaError_t launch_fp64_probe(double* scratch, int blocks, int iters, cudaStream_t st) {
+  fp64_probe_kernel<<<blocks, 256, 0, st>>>(scratch, iters);
   return cudaGetLastError();
 }
 

@@ -78,13 +78,20 @@ cudaError_t launch_forward(const FwdLaunch& a, cudaStream_t st);
 int forward_max_grid(int kind, int threads, int device);
 cudaError_t launch_adjoint(const AdjLaunch& a, cudaStream_t st);
 cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st);
-// L = sqrt(sum_{m>=1} y^2) into *loss (device); scratch >= 1024 doubles.
+// L = sqrt(sum_{m>=1} y^2) into *loss (device); scratch >= 1025 doubles. With a
+// group (world > 1) the sum of squares is summed over ranks first.
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
-                        cudaStream_t st);
+                        const GroupView& g, GridSync* gs, unsigned* status, cudaStream_t st);
+// In-place deterministic sum of v[0..cnt) over the ranks of the group.
+cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cnt, unsigned* status,
+                             cudaStream_t st);
 // grad (device, np) = sum over (m >= 1, b) of w . dh/dp; scratch sized by vjp_scratch_doubles.
 size_t vjp_scratch_doubles(const DevModel& m);
 cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times,
                        const double* wq, int nb, int nt, double* scratch, double* grad,
                        cudaStream_t st);
+
+// 8 * iters DFMA per thread of `blocks` x 256 threads.
+cudaError_t launch_fp64_probe(double* scratch, int blocks, int iters, cudaStream_t st);
 
 }  // namespace cko

@@ -54,7 +54,7 @@ def test_mds_sequential_edge(port):
     """nc = 1 on MDS: early steps converge at iteration 0 (|r0| <= tol_a, SURVEY §7 hard parts)."""
     m = P.build_mass_damper_spring(10, 16)
     y0 = np.zeros((16, 20))
-    t = uniform_times(300, 16, 0.01)
+    t = uniform_times(300, 16, 3e-4)  # dt = 1e-6 as in C2 (nt = 10000, t_max = 0.01)
     want = port.gradient(m, y0, t, 1)
     got = run_gpu(m, y0, t, 1, (0, 1))
     assert got.trajectory.work.as_dict() == want.fwd
