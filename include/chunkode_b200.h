@@ -243,6 +243,12 @@ cko_status cko_ctx_enable_timing(cko_ctx* ctx, int on);
 cko_status cko_ctx_last_kernel_ms(cko_ctx* ctx, double* out4);
 /* Kernel launches made by the last forward / adjoint call (for accounting). */
 int cko_ctx_last_launches(cko_ctx* ctx);
+/* Kernel generation: 2 (default) runs the warp-specialised producer/consumer
+ * Thomas kernels for the state sizes they are instantiated for, 1 forces the
+ * generic per-point kernels everywhere (A/B measurement and cross-checks).
+ * cko_ctx_kernel_generation_used reports what the last forward / adjoint ran. */
+cko_status cko_ctx_set_kernel_generation(cko_ctx* ctx, int gen);
+int cko_ctx_kernel_generation_used(cko_ctx* ctx);
 /* FP64 FMA-pipe throughput probe (dependent-chain-free DFMA stream over all
  * SMs); writes TFLOP/s (2 flops per DFMA). The FP64 roof for the roofline. */
 cko_status cko_probe_fp64_tflops(cko_ctx* ctx, double* tflops, cko_error* err);

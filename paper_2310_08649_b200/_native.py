@@ -62,6 +62,8 @@ def lib() -> C.CDLL:
         "cko_ctx_last_kernel_ms": ([vp, dp], C.c_int),
         "cko_ctx_last_launches": ([vp], C.c_int),
         "cko_probe_fp64_tflops": ([vp, dp, P(E)], C.c_int),
+        "cko_ctx_set_kernel_generation": ([vp, C.c_int], C.c_int),
+        "cko_ctx_kernel_generation_used": ([vp], C.c_int),
         "cko_newton_solve_chunk": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, P(N), P(S), C.c_int, P(C.c_int), P(W),
                                     P(E)], C.c_int),
     }
@@ -82,5 +84,6 @@ EXPORTS = [
     "cko_be_forward", "cko_be_forward_device", "cko_be_adjoint", "cko_be_adjoint_host", "cko_be_adjoint_device",
     "cko_gradient_adjoint", "cko_traj_states", "cko_traj_destroy", "cko_block_bidiag_solve",
     "cko_newton_solve_chunk", "cko_ctx_enable_timing", "cko_ctx_last_kernel_ms", "cko_ctx_last_launches",
-    "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open",
+    "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open", "cko_ctx_set_kernel_generation",
+    "cko_ctx_kernel_generation_used",
 ]

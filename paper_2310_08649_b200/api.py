@@ -195,6 +195,15 @@ class Context:
     def set_stream(self, stream_handle: int):
         lib().cko_ctx_set_stream(self.h, C.c_void_p(stream_handle))
 
+    def set_kernel_generation(self, gen: int):
+        """2 (default): warp-specialised Thomas kernels where instantiated; 1: generic kernels only."""
+        if lib().cko_ctx_set_kernel_generation(self.h, int(gen)) != 0:
+            raise ValueError(f"kernel generation must be 1 or 2, got {gen}")
+
+    def kernel_generation_used(self) -> int:
+        """Kernel generation the last forward / adjoint call ran (1 or 2)."""
+        return int(lib().cko_ctx_kernel_generation_used(self.h))
+
     def model(self, m: Model) -> C.c_void_p:
         key = (m.kind, m.n_unit, m.width, m.n_batch, m.lane_offset, m.params.tobytes())
         dm = self._models.get(key)

@@ -133,10 +133,12 @@ struct cko_ctx {
   // batch sharding
   GroupView grp{};
   // kernel timing (cko_ctx_enable_timing)
+  int kernel_gen = 2;  // 2: warp-specialised Thomas kernels where instantiated; 1: generic kernels only
   bool timing = false;
   cudaEvent_t ev[8] = {};
   double last_ms[4] = {0, 0, 0, 0};
   int last_launches = 0;
+  int last_gen = 0;  // kernel generation the last forward/adjoint call ran
   void mark(int i) {
     if (timing) cudaEventRecord(ev[i], stream);
   }
@@ -237,6 +239,14 @@ cko_status cko_ctx_last_kernel_ms(cko_ctx* c, double* out4) {
 }
 
 int cko_ctx_last_launches(cko_ctx* c) { return c ? c->last_launches : 0; }
+
+cko_status cko_ctx_set_kernel_generation(cko_ctx* c, int gen) {
+  if (!c || (gen != 1 && gen != 2)) return CKO_ERROR;
+  c->kernel_gen = gen;
+  return CKO_OK;
+}
+
+int cko_ctx_kernel_generation_used(cko_ctx* c) { return c ? c->last_gen : 0; }
 
 cko_status cko_probe_fp64_tflops(cko_ctx* c, double* tflops, cko_error* err) {
   if (!c || !tflops) return fail(err, CKO_ERROR, "null argument");
@@ -417,11 +427,24 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   const int n = m->dm.n;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  int maxg = forward_max_grid(m->dm.kind, kThreads, c->device);
-  if (maxg < 1) return fail(err, CKO_CUDA, "forward kernel cannot be made resident");
-  const int G = nb < maxg ? nb : maxg;
+  const bool v2 = !pcr && c->kernel_gen >= 2 && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  int G;
   Slab slab;
-  if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  if (v2) {
+    G = nb < c->sms ? nb : c->sms;
+    slab.Lmax = (nb + G - 1) / G;
+    slab.Pmax = nc_eff * slab.Lmax;
+    slab.doubles = (size_t)slab.Pmax * (n + 1);
+    slab.ints = 0;
+    CUDA_TRY(c->slab.ensure(sizeof(double) * slab.doubles * G));
+    slab.base = c->slab.as<double>();
+    slab.pbase = nullptr;
+  } else {
+    int maxg = forward_max_grid(m->dm.kind, kThreads, c->device);
+    if (maxg < 1) return fail(err, CKO_CUDA, "forward kernel cannot be made resident");
+    G = nb < maxg ? nb : maxg;
+    if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  }
   const int n_chunks = (nt + nc - 1) / nc;
   CUDA_TRY(c->rn.ensure(sizeof(double) * nb));
   CUDA_TRY(c->r0.ensure(sizeof(double) * nb));
@@ -456,9 +479,13 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.grid = G;
   a.threads = kThreads;
   c->mark(0);
-  CUDA_TRY(launch_forward(a, c->stream));
+  if (v2)
+    CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
+  else
+    CUDA_TRY(launch_forward(a, c->stream));
   c->mark(1);
   c->last_launches = 1;
+  c->last_gen = v2 ? 2 : 1;
   int info[4];
   unsigned long long key;
   CUDA_TRY(cudaMemcpyAsync(info, c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
@@ -532,9 +559,11 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   const int n = m->dm.n, np = m->dm.np;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const int G = nb < 2 * c->sms ? nb : 2 * c->sms;
-  Slab slab;
-  if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  const bool v2 = !pcr && c->kernel_gen >= 2 && launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const int G = v2 ? (nb < c->sms ? nb : c->sms) : (nb < 2 * c->sms ? nb : 2 * c->sms);
+  Slab slab{};
+  if (!v2)
+    if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
   const size_t row = (size_t)nb * n;
   CUDA_TRY(c->lambda.ensure(sizeof(double) * row));
   CUDA_TRY(c->wq.ensure(sizeof(double) * row * (nt + 1)));
@@ -549,6 +578,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(c->grad.ensure(sizeof(double) * np));
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
   c->last_launches = 3;
+  c->last_gen = v2 ? 2 : 1;
   c->mark(6);
   if (loss_kind == CKO_LOSS_FROBENIUS) {
     CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
@@ -574,7 +604,10 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.grid = G;
   a.threads = kThreads;
   c->mark(2);
-  CUDA_TRY(launch_adjoint(a, c->stream));
+  if (v2)
+    CUDA_TRY(launch_adjoint_v2(m->dm.kind, n, &a, c->stream));
+  else
+    CUDA_TRY(launch_adjoint(a, c->stream));
   c->mark(3);
   c->mark(4);
   CUDA_TRY(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),

@@ -1,6 +1,7 @@
 // cko_inst.cuh — one translation unit per device model (parallel builds).
 #pragma once
 #include "cko_impl.cuh"
+#include "cko_v2.cuh"
 
 #define CKO_INSTANTIATE(NAME, MD)                                                                      \
   namespace cko {                                                                                     \

@@ -1,3 +1,19 @@
 // Kernel instantiations for the constant model.
 #include "cko_inst.cuh"
 CKO_INSTANTIATE(constant, cko::MConstantRate)
+namespace cko {
+cudaError_t fwd2_run_constant(int n, const FwdLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 1: return v2::fwd2_launch<v2::ConstantRateS>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+cudaError_t adj2_run_constant(int n, const AdjLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 1: return v2::adj2_launch<v2::ConstantRateS>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+}  // namespace cko

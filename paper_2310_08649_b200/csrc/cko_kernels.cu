@@ -11,6 +11,7 @@
 //  vjp_kernel  : sum of w . dh/dp over all points (ode_model.cpp:135-153),
 //                reduced deterministically.
 #include "cko_impl.cuh"
+#include "cko_v2.cuh"
 
 namespace cko {
 
@@ -20,6 +21,12 @@ CKO_DECLARE(lin3)
 CKO_DECLARE(mds)
 CKO_DECLARE(chaboche)
 CKO_DECLARE(node)
+CKO_V2_DECLARE(scalar)
+CKO_V2_DECLARE(constant)
+CKO_V2_DECLARE(lin3)
+CKO_V2_DECLARE(mds)
+CKO_V2_DECLARE(chaboche)
+CKO_V2_DECLARE(node)
 
 size_t slab_doubles_per_point(int n, bool pcr) {
   return 2 * (size_t)n + (size_t)n * n + 1 + (pcr ? 3 * (size_t)n * n + n : 0);
@@ -175,6 +182,18 @@ int forward_max_grid(int kind, int threads, int device) {
 cudaError_t launch_adjoint(const AdjLaunch& a, cudaStream_t st) {
 #define CALL(N) adj_run_##N(a, st)
   CKO_SWITCH(a.m.kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_forward_v2(int kind, int n, const FwdLaunch* a, cudaStream_t st) {
+#define CALL(N) fwd2_run_##N(n, a, st)
+  CKO_SWITCH(kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t st) {
+#define CALL(N) adj2_run_##N(n, a, st)
+  CKO_SWITCH(kind, CALL)
 #undef CALL
 }
 

@@ -78,6 +78,11 @@ cudaError_t launch_forward(const FwdLaunch& a, cudaStream_t st);
 int forward_max_grid(int kind, int threads, int device);
 cudaError_t launch_adjoint(const AdjLaunch& a, cudaStream_t st);
 cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st);
+// v2 warp-specialised Thomas kernels (cko_v2.cuh), one CTA per SM with
+// a.grid CTAs; a == nullptr probes support for (kind, n). Forward needs a
+// slab of Pmax * (n + 1) doubles per CTA (residual rows + point norms).
+cudaError_t launch_forward_v2(int kind, int n, const FwdLaunch* a, cudaStream_t st);
+cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t st);
 // L = sqrt(sum_{m>=1} y^2) into *loss (device); scratch >= 1025 doubles. With a
 // group (world > 1) the sum of squares is summed over ranks first.
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,

@@ -1,0 +1,616 @@
+// cko_v2.cuh — warp-specialised sm_100a kernels for the chunked backward-Euler
+// path with Thomas (block-substitution) solves.
+//
+// Mapping:
+//  * one persistent CTA per SM owns a contiguous lane range; lanes are
+//    processed in tiles of <= LT lanes;
+//  * a Newton iteration of a chunk (integrate.cpp:208-231) or one reversed
+//    chunk of the adjoint (adjoint.cpp:64-101) is an "epoch" over its rows
+//    k = 0..c-1: PRODUCER warps build M_k = I - dt J_k (or its transpose) and
+//    LU-factor it with the rows spread over a group of G lanes (register
+//    resident, logical partial pivoting that reproduces the reference's pivot
+//    sequence, linalg.cpp:13-44); a CONSUMER warp runs the sequential
+//    substitution x_k = M_k^{-1}(r_k + x_{k-1}) one thread per lane. The two
+//    meet in an S-slot shared-memory ring guarded by named barriers, so the
+//    factorisation of rows k+1..k+S overlaps the substitution of row k;
+//  * the forward's all-lanes convergence predicate (integrate.cpp:176-182)
+//    stays the only cross-CTA coupling (grid_reduce_or, cko_common.cuh).
+#pragma once
+#include <cfloat>
+#include <climits>
+
+#include "cko_impl.cuh"
+#include "cko_static_models.cuh"
+
+namespace cko {
+namespace v2 {
+
+// Rows of an N x N block are spread over G lanes, R rows per lane
+// (row i -> lane i % G, slot i / G); GPW groups per warp.
+template <int N>
+struct Geo {
+  static constexpr int G = N <= 8 ? 1 : (N <= 16 ? 8 : (N <= 20 ? 10 : 16));
+  static constexpr int R = (N + G - 1) / G;
+  static constexpr int GPW = 32 / G;
+};
+
+constexpr int kSlots = 3;  // ring depth (10 warps at Ws = 3: <= 168 registers per thread)
+constexpr int kMaxWs = 3;  // producer warps per slot
+
+// Shared-memory record of one factored point (doubles): LU rows in the
+// reference's row order, 1/U_ii, rhs (adjoint), dt, permutation (ints).
+// The stride is padded to 2 mod 16 doubles so the consumer threads' same-offset
+// 16-byte loads of different records fall in different bank groups.
+template <int N>
+struct Rec {
+  static constexpr int LU = 0;
+  static constexpr int RD = N * N;
+  static constexpr int RHS = RD + N;
+  static constexpr int DT = RHS + N;
+  static constexpr int PERM = DT + 1;                       // ints start here (as double offset)
+  static constexpr int RAW = PERM + (N + 1) / 2;
+  static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
+};
+
+struct Shape {
+  int S, Ws, LT;       // slots, producer warps per slot, lanes per tile
+  int threads;
+  int smem_bytes;
+};
+
+template <class MS>
+__host__ __device__ inline void smem_layout(int S, int Ws, int LT, int& o_cs, int& o_rec, int& o_pb, int& o_vs,
+                                            int& o_lam, int& total_doubles) {
+  constexpr int N = MS::N;
+  o_cs = 0;
+  o_rec = ((MS::NCONST + 1) / 2) * 2;
+  o_pb = o_rec + S * LT * Rec<N>::STRIDE;
+  const int groups = S * Ws * Geo<N>::GPW;
+  o_vs = o_pb + groups * 2 * N;
+  o_lam = o_vs + LT * N + (N & 1);
+  total_doubles = o_lam + LT * N + 8;
+}
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// max over the group of a non-negative double (bit order == value order)
+__device__ __forceinline__ double group_max_nonneg(unsigned gmask, double v) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+  const unsigned mh = __reduce_max_sync(gmask, hi);
+  const unsigned ml = __reduce_max_sync(gmask, hi == mh ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+}
+
+// LU with partial pivoting (lu_factor_block, linalg.cpp:13-44) of the block
+// whose rows lane gl of a G-lane group holds in a[s] (row gl + s G). Rows never
+// move: pos[s] tracks each row's position in the reference's swapped order and
+// the pivot of column c is the candidate (pos >= c) with the largest |a|,
+// ties to the smallest position — exactly the reference's strict '>' scan.
+// Factors go to `rec` in reference row order; pb is a 2N-double group buffer.
+template <int N>
+__device__ inline bool lu_group(double (&a)[Geo<N>::R][N], unsigned gmask, int gl, double* pb, double* rec) {
+  constexpr int G = Geo<N>::G, R = Geo<N>::R;
+  int pos[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) pos[s] = (gl + s * G < N) ? gl + s * G : -1;
+  double lm = 0.0;
+#pragma unroll
+  for (int s = 0; s < R; ++s)
+    if (pos[s] >= 0)
+#pragma unroll
+      for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
+  const double tiny = 1e-14 * group_max_nonneg(gmask, lm);
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    unsigned bh = 0, bl = 0, bp = 0xffffffffu;
+    bool have = false;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (pos[s] >= c) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(a[s][c]));
+        const unsigned h = (unsigned)(bits >> 32), l = (unsigned)bits, p = (unsigned)pos[s];
+        const bool better = !have || h > bh || (h == bh && (l > bl || (l == bl && p < bp)));
+        if (better) bh = h, bl = l, bp = p, have = true;
+      }
+    }
+    const unsigned mh = __reduce_max_sync(gmask, have ? bh : 0u);
+    const unsigned ml = __reduce_max_sync(gmask, (have && bh == mh) ? bl : 0u);
+    const int p = (int)__reduce_min_sync(gmask, (have && bh == mh && bl == ml) ? bp : 0xffffffffu);
+    double* buf = pb + (c & 1) * N;
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if (pos[s] == p)
+#pragma unroll
+        for (int j = c; j < N; ++j) buf[j] = a[s][j];
+    __syncwarp(gmask);
+    const double piv = buf[c];
+    if (fabs(piv) < tiny || piv == 0.0) ok = false;
+    const double inv = 1.0 / piv;
+    if (gl == 0) rec[Rec<N>::RD + c] = inv;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (pos[s] == p)
+        pos[s] = c;
+      else if (pos[s] == c)
+        pos[s] = p;
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (pos[s] > c) {
+        const double l = a[s][c] * inv;
+        a[s][c] = l;
+#pragma unroll
+        for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+      }
+    }
+  }
+  int* perm = reinterpret_cast<int*>(rec + Rec<N>::PERM);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (pos[s] >= 0) {
+      double* row = rec + pos[s] * N;
+#pragma unroll
+      for (int j = 0; j < N; ++j) row[j] = a[s][j];
+      perm[pos[s]] = gl + s * G;
+    }
+  }
+  return ok;
+}
+
+// lu_solve_vec (linalg.cpp:46-60) from a record, one thread: v <- M^{-1} v.
+// vs is this thread's N-double scratch for the permuted gather.
+template <int N>
+__device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* vs, double (&v)[N]) {
+  const double* rec = static_cast<const double*>(__builtin_assume_aligned(rec_in, 16));
+  const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
+#pragma unroll
+  for (int i = 0; i < N; ++i) vs[i] = v[i];
+  double y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) y[i] = vs[perm[i]];
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    double s = y[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) s -= rec[i * N + j] * y[j];
+    y[i] = s;
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    double s = y[i];
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) s -= rec[i * N + j] * y[j];
+    y[i] = s * rec[Rec<N>::RD + i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = y[i];
+}
+
+template <int N>
+__device__ __forceinline__ void load_vec(const double* __restrict__ p, double (&v)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = p[i];
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+struct FwdCtx {
+  int lb0, L, step, c;
+  size_t row;  // nb * N
+};
+
+// Residual + lane norms for all c x L points of this CTA (rate_residual_norms,
+// integrate.cpp:64-95). The chunk's iterate yy_k lives in its final place,
+// trajectory row step + 1 + k, so yy_{-1} = y_start is row `step`.
+template <class MS>
+__device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double* cs, double* hr, double* nrm,
+                              bool first, unsigned* s_flags) {
+  constexpr int N = MS::N;
+  const int nb = a.nb;
+  for (int p = threadIdx.x; p < x.c * x.L; p += blockDim.x) {
+    const int k = p / x.L, lb = p % x.L, b = x.lb0 + lb;
+    const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+    const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+    double y[N], ym[N], h[N];
+    load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
+    load_vec<N>(a.states + (size_t)(x.step + k) * x.row + (size_t)b * N, ym);
+    MS::rate(a.m, cs, t, y, h, b);
+    double s = 0.0;
+    double* o = hr + (size_t)p * N;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
+      o[i] = v;
+      s = xadd(s, xmul(v, v));
+    }
+    nrm[p] = s;
+  }
+  if (threadIdx.x == 0) *s_flags = 0;
+  __syncthreads();
+  unsigned f = 0;
+  for (int lb = threadIdx.x; lb < x.L; lb += blockDim.x) {
+    const int b = x.lb0 + lb;
+    double acc = 0.0;
+    for (int k = 0; k < x.c; ++k) acc = xadd(acc, nrm[k * x.L + lb]);
+    const double rn = sqrt(acc);
+    double r0v;
+    if (first) {
+      a.r0[b] = rn;
+      r0v = rn;
+    } else {
+      r0v = a.r0[b];
+    }
+    a.rn[b] = rn;
+    if (!isfinite(rn)) f |= FLAG_NON_FINITE;
+    if (!(rn <= a.tol_a || rn <= xmul(a.tol_r, r0v))) f |= FLAG_NOT_CONVERGED;
+  }
+  if (f) atomicOr(s_flags, f);
+  __syncthreads();
+  return *s_flags;
+}
+
+// One Newton iteration over the rows of one lane tile (integrate.cpp:208-231).
+template <class MS>
+__device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, const double* cs, double* recs,
+                          double* pbs, double* vss, const double* hr, int t0, int LTc, unsigned* s_sing) {
+  constexpr int N = MS::N;
+  using Gm = Geo<N>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = sh.S, Ws = sh.Ws;
+  const int nthr = 32 * (Ws + 1);
+  const int nb = a.nb;
+  if (warp < S * Ws) {
+    // ---- producer: J -> M = I - J dt -> LU for rows k = s, s + S, ...
+    const int s = warp / Ws, sw = warp % Ws;
+    const int g = lane / Gm::G, gl = lane % Gm::G;
+    const int lt = sw * Gm::GPW + g;
+    const bool active = g < Gm::GPW && lt < LTc;
+    const unsigned gmask = (Gm::G == 32) ? 0xffffffffu : (((1u << Gm::G) - 1u) << (g * Gm::G));
+    double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
+    for (int k = s; k < x.c; k += S) {
+      if (k >= S) bar_sync(1 + S + s, nthr);
+      if (active) {
+        const int lb = t0 + lt, b = x.lb0 + lb;
+        double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+        const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+        double y[N];
+        load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
+        double m[Gm::R][N];
+        const double ndt = -dt;
+#pragma unroll
+        for (int r = 0; r < Gm::R; ++r) {
+          const int i = gl + r * Gm::G;
+          if (i < N) {
+            MS::jac_row(a.m, cs, t, y, i, m[r], b);
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+              m[r][j] = xmul(ndt, m[r][j]);
+              if (j == i) m[r][j] = xadd(m[r][j], 1.0);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) m[r][j] = 0.0;
+          }
+        }
+        if (!lu_group<N>(m, gmask, gl, pb, rec)) {
+          if (gl == 0) {
+            atomicMin(a.sing_key, (unsigned long long)k * nb + b);
+            atomicOr(s_sing, 1u);
+          }
+        }
+      }
+      bar_arrive(1 + s, nthr);
+    }
+  } else if (warp == S * Ws) {
+    // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, one thread per lane
+    const int lt = lane;
+    const bool active = lt < LTc;
+    const int lb = t0 + lt, b = x.lb0 + lb;
+    double xv[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) xv[i] = 0.0;
+    double* vs = vss + (size_t)lt * N;
+    for (int k = 0; k < x.c; ++k) {
+      const int s = k % S;
+      bar_sync(1 + s, nthr);
+      if (active) {
+        const double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const double* r = hr + (size_t)(k * x.L + lb) * N;
+        double v[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = r[i] + xv[i];
+        lu_solve_rec<N>(rec, vs, v);
+        double* yy = a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          xv[i] = v[i];
+          yy[i] = yy[i] - v[i];
+        }
+      }
+      if (k + S < x.c) bar_arrive(1 + S + s, nthr);
+    }
+  }
+}
+
+template <class MS>
+__global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) fwd2_kernel(FwdLaunch a, Shape sh) {
+  constexpr int N = MS::N;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned s_bcast, s_flags, s_sing;
+  int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
+  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  double* cs = smem + o_cs;
+  double* recs = smem + o_rec;
+  double* pbs = smem + o_pb;
+  double* vss = smem + o_vs;
+  MS::load_consts(a.m, cs);
+  if (threadIdx.x == 0) s_sing = 0;
+  FwdCtx x;
+  lane_range(a.nb, x.lb0, x.L);
+  x.row = (size_t)a.nb * N;
+  double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
+  double* nrm = hr + (size_t)a.slab.Pmax * N;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  __syncthreads();
+  int step = 0, chunk = 0;
+  while (step < a.nt) {
+    const int c = min(a.nc, a.nt - step);
+    x.step = step;
+    x.c = c;
+    for (int p = threadIdx.x; p < c * x.L; p += blockDim.x) {  // initial iterate: every row at y_start
+      const int k = p / x.L, b = x.lb0 + p % x.L;
+      const double* src = a.states + (size_t)step * x.row + (size_t)b * N;
+      double* dst = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
+      if (a.dy_init) {
+        const double* d = a.dy_init + ((size_t)k * a.nb + b) * N;
+        for (int i = 0; i < N; ++i) dst[i] = src[i] + d[i];
+      } else {
+        for (int i = 0; i < N; ++i) dst[i] = src[i];
+      }
+    }
+    __syncthreads();
+    int it = 0;
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags);
+    f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
+    if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
+      if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
+      return;
+    }
+    while (f & FLAG_NOT_CONVERGED) {
+      if (it == a.max_iter) {
+        if (leader) a.info[0] = 2, a.info[1] = step + 1, a.info[2] = a.max_iter;
+        return;
+      }
+      ++it;
+      for (int t0 = 0; t0 < x.L; t0 += sh.LT) {
+        fwd_epoch<MS>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
+        __syncthreads();
+      }
+      const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
+      f = residual2<MS>(a, x, cs, hr, nrm, false, &s_flags) | fl;
+      f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
+      if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
+        if (leader) {
+          a.info[0] = (f & FLAG_TIMEOUT) ? 4 : (f & FLAG_SINGULAR) ? 1 : 2;
+          a.info[1] = step + 1;
+          a.info[2] = it;
+        }
+        return;
+      }
+    }
+    if (leader) a.iters[chunk] = it;
+    step += c;
+    ++chunk;
+    __syncthreads();
+  }
+  if (leader) a.info[3] = chunk;
+}
+
+// ---------------------------------------------------------------------------
+// adjoint
+// ---------------------------------------------------------------------------
+// One reversed chunk of one lane tile (be_chunk_core, adjoint.cpp:49-127):
+// rows r <-> steps m = step_hi - r. Producers: J(y_m) -> rhs_r = dL_m +
+// dt J^T lambda_c, M_r = (I - J dt)^T, LU. Consumer: delta_r = M_r^{-1}(rhs_r +
+// delta_{r-1}), quadrature weight w_m = (lambda_c + delta_r) dt, and the new
+// carry lambda_c += delta_{c-1}.
+template <class MS>
+__device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs, double* recs, double* pbs,
+                          double* vss, double* lam, int lb0, int t0, int LTc, int step_hi, int c, double Lval,
+                          unsigned long long ord, double (&dcar)[MS::N]) {
+  constexpr int N = MS::N;
+  using Gm = Geo<N>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = sh.S, Ws = sh.Ws;
+  const int nthr = 32 * (Ws + 1);
+  const int nb = a.nb;
+  const size_t row = (size_t)nb * N;
+  if (warp < S * Ws) {
+    const int s = warp / Ws, sw = warp % Ws;
+    const int g = lane / Gm::G, gl = lane % Gm::G;
+    const int lt = sw * Gm::GPW + g;
+    const bool active = g < Gm::GPW && lt < LTc;
+    const unsigned gmask = (Gm::G == 32) ? 0xffffffffu : (((1u << Gm::G) - 1u) << (g * Gm::G));
+    double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
+    for (int r = s; r < c; r += S) {
+      if (r >= S) bar_sync(1 + S + s, nthr);
+      if (active) {
+        const int b = lb0 + t0 + lt, m = step_hi - r;
+        double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const double t = a.times[(size_t)m * nb + b];
+        const double dt = t - a.times[(size_t)(m - 1) * nb + b];
+        double y[N];
+        const double* ym = a.states + (size_t)m * row + (size_t)b * N;
+        load_vec<N>(ym, y);
+        // J rows into the record (scratch), then read back transposed
+#pragma unroll
+        for (int q = 0; q < Gm::R; ++q) {
+          const int i = gl + q * Gm::G;
+          if (i < N) {
+            double jr[N];
+            MS::jac_row(a.m, cs, t, y, i, jr, b);
+#pragma unroll
+            for (int j = 0; j < N; ++j) rec[i * N + j] = jr[j];
+          }
+        }
+        __syncwarp(gmask);
+        const double* lm = lam + (size_t)lt * N;
+        double mt[Gm::R][N];
+#pragma unroll
+        for (int q = 0; q < Gm::R; ++q) {
+          const int i = gl + q * Gm::G;
+          if (i < N) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) mt[q][j] = rec[j * N + i];  // J[j][i]
+            double tmp = 0.0;                                      // (J^T lambda)_i (gemv_transpose)
+#pragma unroll
+            for (int j = 0; j < N; ++j) tmp += mt[q][j] * lm[j];
+            const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? y[i] / Lval : 0.0);
+            rec[Rec<N>::RHS + i] = dl + dt * tmp;
+#pragma unroll
+            for (int j = 0; j < N; ++j) mt[q][j] = (j == i) ? 1.0 - dt * mt[q][j] : -dt * mt[q][j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+          }
+        }
+        if (gl == 0) rec[Rec<N>::DT] = dt;
+        __syncwarp(gmask);
+        if (!lu_group<N>(mt, gmask, gl, pb, rec) && gl == 0)
+          atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
+      }
+      bar_arrive(1 + s, nthr);
+    }
+  } else if (warp == S * Ws) {
+    const int lt = lane;
+    const bool active = lt < LTc;
+    const int b = lb0 + t0 + lt;
+    double* vs = vss + (size_t)lt * N;
+    const double* lc = lam + (size_t)lt * N;
+    double d[N];  // delta_{r-1}, then delta_r
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = 0.0;
+    for (int r = 0; r < c; ++r) {
+      const int s = r % S;
+      bar_sync(1 + s, nthr);
+      if (active) {
+        const double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const int m = step_hi - r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[i] = rec[Rec<N>::RHS + i] + d[i];
+        const double dt = rec[Rec<N>::DT];
+        lu_solve_rec<N>(rec, vs, d);
+        double* w = a.wq + (size_t)m * row + (size_t)b * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
+      }
+      if (r + S < c) bar_arrive(1 + S + s, nthr);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) dcar[i] = d[i];
+  }
+}
+
+template <class MS>
+__global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) adj2_kernel(AdjLaunch a, Shape sh) {
+  constexpr int N = MS::N;
+  extern __shared__ __align__(16) double smem[];
+  int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
+  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  double* cs = smem + o_cs;
+  double* recs = smem + o_rec;
+  double* pbs = smem + o_pb;
+  double* vss = smem + o_vs;
+  double* lam = smem + o_lam;
+  MS::load_consts(a.m, cs);
+  int lb0, L;
+  lane_range(a.nb, lb0, L);
+  const double Lval = a.loss ? *a.loss : 0.0;
+  const int consumer = threadIdx.x >> 5 == sh.S * sh.Ws;
+  const int lane = threadIdx.x & 31;
+  for (int t0 = 0; t0 < L; t0 += sh.LT) {
+    const int LTc = min(sh.LT, L - t0);
+    for (int i = threadIdx.x; i < LTc * N; i += blockDim.x) lam[i] = 0.0;
+    __syncthreads();
+    int step_hi = a.nt;
+    unsigned long long ord = 0;
+    while (step_hi >= 1) {
+      const int c = min(a.nc, step_hi);
+      double dcar[N];
+      adj_epoch<MS>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
+      __syncthreads();
+      if (consumer && lane < LTc) {  // new carry (adjoint.cpp:121-126)
+#pragma unroll
+        for (int i = 0; i < N; ++i) lam[(size_t)lane * N + i] += dcar[i];
+      }
+      __syncthreads();
+      step_hi -= c;
+      ++ord;
+    }
+    for (int i = threadIdx.x; i < LTc * N; i += blockDim.x)
+      a.lambda[(size_t)(lb0 + t0) * N + i] = lam[i];
+    __syncthreads();
+  }
+}
+
+// Launch shape: producer warps per slot cover one step of a lane tile.
+template <class MS>
+inline Shape make_shape(int L) {
+  constexpr int N = MS::N;
+  Shape sh;
+  sh.S = kSlots;
+  const int gpw = Geo<N>::GPW;
+  int Ws = (L + gpw - 1) / gpw;
+  if (Ws > kMaxWs) Ws = kMaxWs;
+  if (Ws < 1) Ws = 1;
+  sh.Ws = Ws;
+  sh.LT = Ws * gpw < 32 ? Ws * gpw : 32;
+  if (sh.LT > L && L >= 1) sh.LT = L;
+  sh.threads = 32 * (sh.S * sh.Ws + 1);
+  int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
+  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  sh.smem_bytes = tot * 8;
+  return sh;
+}
+
+template <class MS>
+cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
+  if (!a) return cudaSuccess;
+  const int Lmax = (a->nb + a->grid - 1) / a->grid;
+  Shape sh = make_shape<MS>(Lmax);
+  cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes);
+  if (e != cudaSuccess) return e;
+  FwdLaunch copy = *a;
+  void* args[] = {&copy, &sh};
+  return cudaLaunchCooperativeKernel((const void*)fwd2_kernel<MS>, dim3(a->grid), dim3(sh.threads), args,
+                                     sh.smem_bytes, st);
+}
+
+template <class MS>
+cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
+  if (!a) return cudaSuccess;
+  const int Lmax = (a->nb + a->grid - 1) / a->grid;
+  Shape sh = make_shape<MS>(Lmax);
+  cudaError_t e = cudaFuncSetAttribute(adj2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes);
+  if (e != cudaSuccess) return e;
+  adj2_kernel<MS><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
+  return cudaGetLastError();
+}
+
+}  // namespace v2
+
+// Per-model v2 launchers (cko_inst_*.cu), dispatching on the state size n;
+// a == nullptr probes support. cudaErrorNotSupported when n has no
+// instantiation (the v1 kernels then run).
+#define CKO_V2_DECLARE(NAME)                                                    \
+  cudaError_t fwd2_run_##NAME(int n, const FwdLaunch* a, cudaStream_t st);      \
+  cudaError_t adj2_run_##NAME(int n, const AdjLaunch* a, cudaStream_t st);
+
+}  // namespace cko
