@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -478,6 +479,13 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.budget_ns = 60ull * 1000 * 1000 * 1000;
   a.grid = G;
   a.threads = kThreads;
+  static const char* trace_path = std::getenv("CKO_TRACE");
+  Buf tbuf;
+  if (trace_path && v2) {
+    CUDA_TRY(tbuf.ensure(sizeof(unsigned long long) * (64 + 8 * (size_t)nc_eff)));
+    CUDA_TRY(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, c->stream));
+    a.trace = tbuf.as<unsigned long long>();
+  }
   c->mark(0);
   if (v2)
     CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
@@ -494,6 +502,15 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   CUDA_TRY(cudaMemcpyAsync(c->iters_host.data(), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (a.trace) {
+    std::vector<unsigned long long> h(tbuf.bytes / sizeof(unsigned long long));
+    CUDA_TRY(cudaMemcpy(h.data(), tbuf.p, tbuf.bytes, cudaMemcpyDeviceToHost));
+    if (FILE* fp = std::fopen(trace_path, "wb")) {
+      std::fwrite(h.data(), sizeof(unsigned long long), h.size(), fp);
+      std::fclose(fp);
+    }
+    tbuf.release();
+  }
   c->last_ms[1] = c->last_ms[2] = c->last_ms[3] = 0.0;
   c->collect(0, 1);
   const int off = m->desc.lane_offset;

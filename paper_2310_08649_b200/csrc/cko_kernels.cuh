@@ -42,6 +42,7 @@ struct FwdLaunch {
   unsigned long long* sing_key;  // min over k * nb + b of singular blocks
   int* info;             // [0] status, [1] chunk_start_step, [2] iterations, [3] n_chunks done
   uint64_t budget_ns;
+  unsigned long long* trace;  // optional diagnostics (CKO_TRACE): per-row timestamps of CTA 0
   int grid;               // CTAs
   int threads;
 };

@@ -26,7 +26,9 @@ namespace cko {
 namespace v2 {
 
 // Rows of an N x N block are spread over G lanes, R rows per lane
-// (row i -> lane i % G, slot i / G); GPW groups per warp.
+// (row i -> lane i % G, slot i / G); GPW groups per warp. Lanes past GPW * G
+// (G = 10: lanes 30, 31) shadow the last group's first lanes: they compute the
+// same values and write the same addresses, which keeps the warp converged.
 template <int N>
 struct Geo {
   static constexpr int G = N <= 8 ? 1 : (N <= 16 ? 8 : (N <= 20 ? 10 : 16));
@@ -34,11 +36,27 @@ struct Geo {
   static constexpr int GPW = 32 / G;
 };
 
-constexpr int kSlots = 3;  // ring depth (10 warps at Ws = 3: <= 168 registers per thread)
-constexpr int kMaxWs = 3;  // producer warps per slot
+// Lane roles inside a warp of producer groups.
+template <int N>
+struct GroupLane {
+  int g, gl, base;
+  __device__ explicit GroupLane(int lane) {
+    constexpr int G = Geo<N>::G, GPW = Geo<N>::GPW;
+    g = lane / G;
+    gl = lane % G;
+    if (g >= GPW) g = GPW - 1;
+    base = g * G;
+  }
+};
 
-// Shared-memory record of one factored point (doubles): LU rows in the
-// reference's row order, 1/U_ii, rhs (adjoint), dt, permutation (ints).
+constexpr int kMaxWarps = 10;  // <= 3 warps per SMSP: up to 168 registers per thread
+constexpr int kMaxSlots = 7;  // named barriers 1..2S must stay below 16
+constexpr int kMaxWs = 3;     // producer warps per slot
+
+// Shared-memory record of one factored point (doubles): the LU factors in
+// the reference's row order (row-major), 1/U_ii, rhs (residual / adjoint
+// rhs), the iterate (forward), dt, and the row permutation (ints; PERM[N] = 1
+// when it is the identity).
 // The stride is padded to 2 mod 16 doubles so the consumer threads' same-offset
 // 16-byte loads of different records fall in different bank groups.
 template <int N>
@@ -46,9 +64,10 @@ struct Rec {
   static constexpr int LU = 0;
   static constexpr int RD = N * N;
   static constexpr int RHS = RD + N;
-  static constexpr int DT = RHS + N;
+  static constexpr int Y = RHS + N;
+  static constexpr int DT = Y + N;
   static constexpr int PERM = DT + 1;                       // ints start here (as double offset)
-  static constexpr int RAW = PERM + (N + 1) / 2;
+  static constexpr int RAW = PERM + (N + 2) / 2;
   static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
 };
 
@@ -76,13 +95,19 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// max over the group of a non-negative double (bit order == value order)
-__device__ __forceinline__ double group_max_nonneg(unsigned gmask, double v) {
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-  const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
-  const unsigned mh = __reduce_max_sync(gmask, hi);
-  const unsigned ml = __reduce_max_sync(gmask, hi == mh ? lo : 0u);
-  return __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+// Rotation reduction inside a group of G lanes starting at lane `base`:
+// after steps 1, 2, 4, ... every lane has combined a window of >= G lanes
+// (idempotent ops only: max / argmax). Works for any G, not just powers of 2.
+template <int G>
+__device__ __forceinline__ int rot_src(int base, int gl, int off) {
+  return base + (gl + off) % G;
+}
+
+template <int G>
+__device__ __forceinline__ double group_max_nonneg(double v, int base, int gl) {
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) v = fmax(v, __shfl_sync(0xffffffffu, v, rot_src<G>(base, gl, off)));
+  return v;
 }
 
 // LU with partial pivoting (lu_factor_block, linalg.cpp:13-44) of the block
@@ -90,9 +115,10 @@ __device__ __forceinline__ double group_max_nonneg(unsigned gmask, double v) {
 // move: pos[s] tracks each row's position in the reference's swapped order and
 // the pivot of column c is the candidate (pos >= c) with the largest |a|,
 // ties to the smallest position — exactly the reference's strict '>' scan.
-// Factors go to `rec` in reference row order; pb is a 2N-double group buffer.
+// The whole warp must call this (shuffles use the full mask); factors go to
+// `rec` in reference row order; pb is a 2N-double group buffer.
 template <int N>
-__device__ inline bool lu_group(double (&a)[Geo<N>::R][N], unsigned gmask, int gl, double* pb, double* rec) {
+__device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec) {
   constexpr int G = Geo<N>::G, R = Geo<N>::R;
   int pos[R];
 #pragma unroll
@@ -103,34 +129,50 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], unsigned gmask, int g
     if (pos[s] >= 0)
 #pragma unroll
       for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
-  const double tiny = 1e-14 * group_max_nonneg(gmask, lm);
+  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
   bool ok = true;
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    unsigned bh = 0, bl = 0, bp = 0xffffffffu;
-    bool have = false;
+    // key (|a|, position): larger |a| wins, ties to the smaller position
+    double bv = -1.0;
+    int bp = INT_MAX, bs = 0;
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       if (pos[s] >= c) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(a[s][c]));
-        const unsigned h = (unsigned)(bits >> 32), l = (unsigned)bits, p = (unsigned)pos[s];
-        const bool better = !have || h > bh || (h == bh && (l > bl || (l == bl && p < bp)));
-        if (better) bh = h, bl = l, bp = p, have = true;
+        const double v = fabs(a[s][c]);
+        if (v > bv || (v == bv && pos[s] < bp)) bv = v, bp = pos[s], bs = s;
       }
     }
-    const unsigned mh = __reduce_max_sync(gmask, have ? bh : 0u);
-    const unsigned ml = __reduce_max_sync(gmask, (have && bh == mh) ? bl : 0u);
-    const int p = (int)__reduce_min_sync(gmask, (have && bh == mh && bl == ml) ? bp : 0xffffffffu);
+    int own = bp;  // my best candidate's position (INT_MAX if none)
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+      const int src = rot_src<G>(base, gl, off);
+      const double ov = __shfl_sync(0xffffffffu, bv, src);
+      const int op = __shfl_sync(0xffffffffu, bp, src);
+      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
+    }
+    int p = bp;
+    if (p == INT_MAX) {  // no comparable candidate (NaN column): keep row c, flag it
+      p = c;
+      ok = false;
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if (pos[s] == c) own = c, bs = s;
+    }
     double* buf = pb + (c & 1) * N;
+    if (own == p) {  // the owner lane publishes the pivot row from slot bs
 #pragma unroll
-    for (int s = 0; s < R; ++s)
-      if (pos[s] == p)
+      for (int j = c; j < N; ++j) {
+        double u = a[0][j];
 #pragma unroll
-        for (int j = c; j < N; ++j) buf[j] = a[s][j];
-    __syncwarp(gmask);
+        for (int s = 1; s < R; ++s) u = (bs == s) ? a[s][j] : u;
+        buf[j] = u;
+      }
+    }
+    __syncwarp();
     const double piv = buf[c];
     if (fabs(piv) < tiny || piv == 0.0) ok = false;
-    const double inv = 1.0 / piv;
+    const double inv = __drcp_rn(piv);  // == 1.0 / piv, correctly rounded
     if (gl == 0) rec[Rec<N>::RD + c] = inv;
 #pragma unroll
     for (int s = 0; s < R; ++s) {
@@ -159,33 +201,139 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], unsigned gmask, int g
       perm[pos[s]] = gl + s * G;
     }
   }
+  if (gl == 0) perm[N] = 0;
+  return ok;
+}
+
+// Fast path of lu_group: the same elimination without the pivot search, for
+// blocks where the reference's scan keeps every diagonal (|a(r,c)| <= |a(c,c)|
+// for all r > c, the common case for M = I - dt J). The row of column c then
+// sits at a static lane/slot, so there is no argmax and no select; `viol`
+// reports (per lane) whether the reference would have exchanged rows, in which
+// case the caller redoes the block with lu_group. When no exchange happens the
+// arithmetic is identical to lu_group / lu_factor_block.
+template <int N>
+__device__ inline bool lu_group_nopiv(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec,
+                                      bool& viol) {
+  constexpr int G = Geo<N>::G, R = Geo<N>::R;
+  double lm = 0.0;
+#pragma unroll
+  for (int s = 0; s < R; ++s)
+    if (gl + s * G < N)
+#pragma unroll
+      for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
+  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
+  bool ok = true;
+  viol = false;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double* buf = pb + (c & 1) * N;
+    if (gl == c % G) {
+#pragma unroll
+      for (int j = c; j < N; ++j) buf[j] = a[c / G][j];
+    }
+    __syncwarp();
+    const double piv = buf[c];
+    const double apiv = fabs(piv);
+    if (apiv < tiny || piv == 0.0) ok = false;
+    const double inv = __drcp_rn(piv);
+    if (gl == 0) rec[Rec<N>::RD + c] = inv;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (gl + s * G > c && gl + s * G < N) {
+        const double v = a[s][c];
+        viol |= fabs(v) > apiv;
+        const double l = v * inv;
+        a[s][c] = l;
+#pragma unroll
+        for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+      }
+    }
+  }
+  int* perm = reinterpret_cast<int*>(rec + Rec<N>::PERM);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int i = gl + s * G;
+    if (i < N) {
+      double* row = rec + i * N;
+#pragma unroll
+      for (int j = 0; j < N; ++j) row[j] = a[s][j];
+      perm[i] = i;
+    }
+  }
+  if (gl == 0) perm[N] = 1;
+  return ok;
+}
+
+// Build the block with `build(m)` (rows this lane holds) and factor it: the
+// no-exchange fast path first; if any group of the warp needs a row exchange
+// the whole warp rebuilds and runs the pivoting factorisation.
+template <int N, class Build>
+__device__ __noinline__ bool factor_block_pivoting(const Build& build, int gl, int base, double* pb, double* rec) {
+  double m[Geo<N>::R][N];
+  build(m);
+  __syncwarp();
+  return lu_group<N>(m, gl, base, pb, rec);
+}
+
+template <int N, class Build>
+__device__ inline bool factor_block(const Build& build, int gl, int base, double* pb, double* rec) {
+  bool viol, ok;
+  {
+    double m[Geo<N>::R][N];
+    build(m);
+    ok = lu_group_nopiv<N>(m, gl, base, pb, rec, viol);
+  }
+  if (__any_sync(0xffffffffu, viol)) {  // rare: kept out of line so it costs no registers here
+    __syncwarp();
+    ok = factor_block_pivoting<N>(build, gl, base, pb, rec);
+  }
   return ok;
 }
 
 // lu_solve_vec (linalg.cpp:46-60) from a record, one thread: v <- M^{-1} v.
-// vs is this thread's N-double scratch for the permuted gather.
+// Rows go in blocks of B whose multiply-add chains advance together (B
+// independent chains keep the FP64 pipe busy). The forward sweep accumulates
+// each row in the reference's order (j ascending, bit-identical); the backward
+// sweep accumulates j descending so a row's chain can start before the row
+// just below it is final (a rounding-level reordering of the reference's
+// j-ascending sum). vs: this thread's N-double scratch for the permuted gather.
 template <int N>
 __device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* vs, double (&v)[N]) {
+  constexpr int B = 4;
   const double* rec = static_cast<const double*>(__builtin_assume_aligned(rec_in, 16));
   const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
-#pragma unroll
-  for (int i = 0; i < N; ++i) vs[i] = v[i];
   double y[N];
+  if (perm[N]) {
 #pragma unroll
-  for (int i = 0; i < N; ++i) y[i] = vs[perm[i]];
+    for (int i = 0; i < N; ++i) y[i] = v[i];
+  } else {
 #pragma unroll
-  for (int i = 1; i < N; ++i) {
-    double s = y[i];
+    for (int i = 0; i < N; ++i) vs[i] = v[i];
 #pragma unroll
-    for (int j = 0; j < i; ++j) s -= rec[i * N + j] * y[j];
-    y[i] = s;
+    for (int i = 0; i < N; ++i) y[i] = vs[perm[i]];
   }
+  // forward (unit lower): y_i -= L_ij y_j, j ascending
 #pragma unroll
-  for (int i = N - 1; i >= 0; --i) {
-    double s = y[i];
+  for (int lo = 1; lo < N; lo += B) {
+    const int hi = lo + B - 1 < N - 1 ? lo + B - 1 : N - 1;  // block rows lo..hi
 #pragma unroll
-    for (int j = i + 1; j < N; ++j) s -= rec[i * N + j] * y[j];
-    y[i] = s * rec[Rec<N>::RD + i];
+    for (int j = 0; j < hi; ++j)
+#pragma unroll
+      for (int i = lo; i <= hi; ++i)
+        if (j < i) y[i] -= rec[i * N + j] * y[j];
+  }
+  // backward: y_i = (y_i - U_ij y_j (j descending)) / U_ii
+#pragma unroll
+  for (int hi = N - 1; hi >= 0; hi -= B) {
+    const int lo = hi - B + 1 > 0 ? hi - B + 1 : 0;
+#pragma unroll
+    for (int j = N - 1; j >= lo; --j) {
+      if (j <= hi) y[j] *= rec[Rec<N>::RD + j];
+#pragma unroll
+      for (int i = lo; i <= hi; ++i)
+        if (i < j) y[i] -= rec[i * N + j] * y[j];
+    }
   }
 #pragma unroll
   for (int i = 0; i < N; ++i) v[i] = y[i];
@@ -266,46 +414,52 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
   if (warp < S * Ws) {
-    // ---- producer: J -> M = I - J dt -> LU for rows k = s, s + S, ...
+    // ---- producer: J -> M = I - J dt -> LU for rows k = s, s + S, ...; it
+    // also stages r_k and yy_k in the record so the consumer never waits on L2.
     const int s = warp / Ws, sw = warp % Ws;
-    const int g = lane / Gm::G, gl = lane % Gm::G;
+    const GroupLane<N> gr(lane);
+    const int g = gr.g, gl = gr.gl;
     const int lt = sw * Gm::GPW + g;
-    const bool active = g < Gm::GPW && lt < LTc;
-    const unsigned gmask = (Gm::G == 32) ? 0xffffffffu : (((1u << Gm::G) - 1u) << (g * Gm::G));
+    const bool active = lt < LTc;  // inactive groups factor a duplicate point, no side effects
+    const int lb = t0 + (active ? lt : LTc - 1), b = x.lb0 + lb;
     double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
+    double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == 0 && lane == 0) ? a.trace + 64 : nullptr;
     for (int k = s; k < x.c; k += S) {
+      if (tr) tr[k * 8 + 0] = globaltimer_ns();
       if (k >= S) bar_sync(1 + S + s, nthr);
-      if (active) {
-        const int lb = t0 + lt, b = x.lb0 + lb;
-        double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
-        const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
-        const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
-        double y[N];
-        load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
-        double m[Gm::R][N];
-        const double ndt = -dt;
+      if (tr) tr[k * 8 + 1] = globaltimer_ns();
+      const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+      const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      double y[N];
+      load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
+      const double* r = hr + (size_t)(k * x.L + lb) * N;
+      const double ndt = -dt;
+      auto build = [&](double (&m)[Gm::R][N]) {
 #pragma unroll
-        for (int r = 0; r < Gm::R; ++r) {
-          const int i = gl + r * Gm::G;
+        for (int q = 0; q < Gm::R; ++q) {
+          const int i = gl + q * Gm::G;
           if (i < N) {
-            MS::jac_row(a.m, cs, t, y, i, m[r], b);
+            MS::jac_row(a.m, cs, t, y, i, m[q], b);
 #pragma unroll
             for (int j = 0; j < N; ++j) {
-              m[r][j] = xmul(ndt, m[r][j]);
-              if (j == i) m[r][j] = xadd(m[r][j], 1.0);
+              m[q][j] = xmul(ndt, m[q][j]);
+              if (j == i) m[q][j] = xadd(m[q][j], 1.0);
             }
+            rec[Rec<N>::Y + i] = a.states[(size_t)(x.step + 1 + k) * x.row + (size_t)b * N + i];
+            rec[Rec<N>::RHS + i] = r[i];
           } else {
 #pragma unroll
-            for (int j = 0; j < N; ++j) m[r][j] = 0.0;
+            for (int j = 0; j < N; ++j) m[q][j] = 0.0;
           }
         }
-        if (!lu_group<N>(m, gmask, gl, pb, rec)) {
-          if (gl == 0) {
-            atomicMin(a.sing_key, (unsigned long long)k * nb + b);
-            atomicOr(s_sing, 1u);
-          }
-        }
+      };
+      if (tr) tr[k * 8 + 2] = globaltimer_ns();
+      if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0) {
+        atomicMin(a.sing_key, (unsigned long long)k * nb + b);
+        atomicOr(s_sing, 1u);
       }
+      if (tr) tr[k * 8 + 3] = globaltimer_ns();
       bar_arrive(1 + s, nthr);
     }
   } else if (warp == S * Ws) {
@@ -317,30 +471,29 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
 #pragma unroll
     for (int i = 0; i < N; ++i) xv[i] = 0.0;
     double* vs = vss + (size_t)lt * N;
+    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == 0 && lane == 0) ? a.trace + 64 : nullptr;
     for (int k = 0; k < x.c; ++k) {
       const int s = k % S;
+      if (tr) tr[k * 8 + 4] = globaltimer_ns();
       bar_sync(1 + s, nthr);
+      if (tr) tr[k * 8 + 5] = globaltimer_ns();
       if (active) {
         const double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
-        const double* r = hr + (size_t)(k * x.L + lb) * N;
-        double v[N];
 #pragma unroll
-        for (int i = 0; i < N; ++i) v[i] = r[i] + xv[i];
-        lu_solve_rec<N>(rec, vs, v);
+        for (int i = 0; i < N; ++i) xv[i] = rec[Rec<N>::RHS + i] + xv[i];
+        lu_solve_rec<N>(rec, vs, xv);
         double* yy = a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          xv[i] = v[i];
-          yy[i] = yy[i] - v[i];
-        }
+        for (int i = 0; i < N; ++i) yy[i] = rec[Rec<N>::Y + i] - xv[i];
       }
+      if (tr) tr[k * 8 + 6] = globaltimer_ns();
       if (k + S < x.c) bar_arrive(1 + S + s, nthr);
     }
   }
 }
 
 template <class MS>
-__global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) fwd2_kernel(FwdLaunch a, Shape sh) {
+__global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned s_bcast, s_flags, s_sing;
@@ -377,7 +530,10 @@ __global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) fwd2_kernel(Fwd
     }
     __syncthreads();
     int it = 0;
+    unsigned long long* ktr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && chunk < 4) ? a.trace + chunk * 16 : nullptr;
+    if (ktr) ktr[0] = globaltimer_ns();
     unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags);
+    if (ktr) ktr[1] = globaltimer_ns();
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
       if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
@@ -389,13 +545,16 @@ __global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) fwd2_kernel(Fwd
         return;
       }
       ++it;
+      if (ktr && it < 4) ktr[2 + 3 * (it - 1)] = globaltimer_ns();
       for (int t0 = 0; t0 < x.L; t0 += sh.LT) {
         fwd_epoch<MS>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
         __syncthreads();
       }
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
+      if (ktr && it < 4) ktr[3 + 3 * (it - 1)] = globaltimer_ns();
       f = residual2<MS>(a, x, cs, hr, nrm, false, &s_flags) | fl;
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
+      if (ktr && it < 4) ktr[4 + 3 * (it - 1)] = globaltimer_ns();
       if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
         if (leader) {
           a.info[0] = (f & FLAG_TIMEOUT) ? 4 : (f & FLAG_SINGULAR) ? 1 : 2;
@@ -434,22 +593,24 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   const size_t row = (size_t)nb * N;
   if (warp < S * Ws) {
     const int s = warp / Ws, sw = warp % Ws;
-    const int g = lane / Gm::G, gl = lane % Gm::G;
+    const GroupLane<N> gr(lane);
+    const int g = gr.g, gl = gr.gl;
     const int lt = sw * Gm::GPW + g;
-    const bool active = g < Gm::GPW && lt < LTc;
-    const unsigned gmask = (Gm::G == 32) ? 0xffffffffu : (((1u << Gm::G) - 1u) << (g * Gm::G));
+    const bool active = lt < LTc;  // inactive groups factor a duplicate point, no side effects
+    const int ltc = active ? lt : LTc - 1;
+    const int b = lb0 + t0 + ltc;
     double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
+    double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+    const double* lm = lam + (size_t)ltc * N;
     for (int r = s; r < c; r += S) {
       if (r >= S) bar_sync(1 + S + s, nthr);
-      if (active) {
-        const int b = lb0 + t0 + lt, m = step_hi - r;
-        double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
-        const double t = a.times[(size_t)m * nb + b];
-        const double dt = t - a.times[(size_t)(m - 1) * nb + b];
-        double y[N];
-        const double* ym = a.states + (size_t)m * row + (size_t)b * N;
-        load_vec<N>(ym, y);
-        // J rows into the record (scratch), then read back transposed
+      const int m = step_hi - r;
+      const double t = a.times[(size_t)m * nb + b];
+      const double dt = t - a.times[(size_t)(m - 1) * nb + b];
+      double y[N];
+      load_vec<N>(a.states + (size_t)m * row + (size_t)b * N, y);
+      // J rows into the record (scratch), then read back transposed
+      auto build = [&](double (&mt)[Gm::R][N]) {
 #pragma unroll
         for (int q = 0; q < Gm::R; ++q) {
           const int i = gl + q * Gm::G;
@@ -460,9 +621,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
             for (int j = 0; j < N; ++j) rec[i * N + j] = jr[j];
           }
         }
-        __syncwarp(gmask);
-        const double* lm = lam + (size_t)lt * N;
-        double mt[Gm::R][N];
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < Gm::R; ++q) {
           const int i = gl + q * Gm::G;
@@ -472,7 +631,8 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
             double tmp = 0.0;                                      // (J^T lambda)_i (gemv_transpose)
 #pragma unroll
             for (int j = 0; j < N; ++j) tmp += mt[q][j] * lm[j];
-            const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? y[i] / Lval : 0.0);
+            const double yi = a.states[(size_t)m * row + (size_t)b * N + i];
+            const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? yi / Lval : 0.0);
             rec[Rec<N>::RHS + i] = dl + dt * tmp;
 #pragma unroll
             for (int j = 0; j < N; ++j) mt[q][j] = (j == i) ? 1.0 - dt * mt[q][j] : -dt * mt[q][j];
@@ -482,10 +642,10 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
           }
         }
         if (gl == 0) rec[Rec<N>::DT] = dt;
-        __syncwarp(gmask);
-        if (!lu_group<N>(mt, gmask, gl, pb, rec) && gl == 0)
-          atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
-      }
+        __syncwarp();
+      };
+      if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0)
+        atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + s, nthr);
     }
   } else if (warp == S * Ws) {
@@ -519,7 +679,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
 }
 
 template <class MS>
-__global__ void __launch_bounds__(32 * (kSlots * kMaxWs + 1), 1) adj2_kernel(AdjLaunch a, Shape sh) {
+__global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
@@ -565,14 +725,14 @@ template <class MS>
 inline Shape make_shape(int L) {
   constexpr int N = MS::N;
   Shape sh;
-  sh.S = kSlots;
   const int gpw = Geo<N>::GPW;
   int Ws = (L + gpw - 1) / gpw;
   if (Ws > kMaxWs) Ws = kMaxWs;
   if (Ws < 1) Ws = 1;
   sh.Ws = Ws;
-  sh.LT = Ws * gpw < 32 ? Ws * gpw : 32;
-  if (sh.LT > L && L >= 1) sh.LT = L;
+  sh.S = (kMaxWarps - 1) / Ws;  // ring depth: as many slots as the warp budget allows
+  if (sh.S > kMaxSlots) sh.S = kMaxSlots;
+  sh.LT = Ws * gpw < 32 ? Ws * gpw : 32;  // lanes per tile == records per slot
   sh.threads = 32 * (sh.S * sh.Ws + 1);
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
   smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);

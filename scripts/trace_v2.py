@@ -1,0 +1,32 @@
+"""Diagnostics: per-row timeline of CTA 0 in the first chunk of a v2 forward (CKO_TRACE)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+path = "/tmp/cko_trace.bin"
+os.environ["CKO_TRACE"] = path
+import paper_2310_08649_b200 as P  # noqa: E402
+from paper_2310_08649_b200 import api  # noqa: E402
+
+nb, nt, nc = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+m = P.build_mass_damper_spring(10, nb)
+grid = api.TimeGrid.uniform(nt, nb, nt * 1e-6)
+for rep in range(2):
+    api.integrate_backward_euler(m, np.zeros((nb, 20)), grid, nc, solver=api.SolverChoice(0))
+t = np.fromfile(path, dtype=np.uint64).astype(np.int64)
+k0 = t[0]
+print("chunk markers (us from chunk-0 start): res0, [it: epoch-start, epoch-end, res+sync-end]")
+for ch in range(4):
+    row = t[ch * 16: ch * 16 + 11]
+    print(ch, [(v - k0) / 1000 if v else None for v in row])
+rows = t[64:].reshape(-1, 8)
+print("row: prod(wait-start, acquired, lu-start, lu-end) cons(wait-start, acquired, done) in us")
+for k in range(min(nc, 24)):
+    r = rows[k]
+    print(k, " ".join(f"{(v - k0) / 1000:8.2f}" if v else "       -" for v in r[:7]))
+cons = rows[:, 6] - rows[:, 5]
+lu = rows[:, 3] - rows[:, 2]
+print("consumer solve us: median %.3f; producer LU us: median %.3f; producer load us: median %.3f" % (
+    np.median(cons[cons > 0]) / 1000, np.median(lu[lu > 0]) / 1000, np.median((rows[:, 2] - rows[:, 1])[lu > 0]) / 1000))
