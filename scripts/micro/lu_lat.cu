@@ -10,17 +10,23 @@ __global__ void k_lu(int iters, long long* out, double* sink) {
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GroupLane<N> gr(lane);
-  double* pb = sm + (warp * Gm::GPW + gr.g) * 2 * N;
-  double* rec = sm + 27 * 2 * N + (warp * Gm::GPW + gr.g) * Rec<N>::STRIDE;
-  long long t0 = clock64();
+  __shared__ double init[N * N];
+  for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+    const int i = e / N, j = e % N;
+    init[e] = (i == j) ? 1.0 : 0.01 * ((i * 7 + j * 3) % 11) - 0.05;
+  }
+  __syncthreads();
+  double* pb = sm + (warp * Gm::GPW + gr.g) * 2 * (N + 2);
+  double* rec = sm + 27 * 2 * (N + 2) + (warp * Gm::GPW + gr.g) * Rec<N>::STRIDE;
   bool okall = true;
+  long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     double m[Gm::R][N];
 #pragma unroll
     for (int q = 0; q < Gm::R; ++q) {
       const int i = gr.gl + q * Gm::G;
 #pragma unroll
-      for (int j = 0; j < N; ++j) m[q][j] = (i == j) ? 1.0 + 1e-3 * it : 0.01 * ((i * 7 + j * 3) % 11) - 0.05;
+      for (int j = 0; j < N; ++j) m[q][j] = init[(i < N ? i : 0) * N + j];
     }
     bool viol;
     okall &= lu_group_nopiv<N>(m, gr.gl, gr.base, pb, rec, viol);
@@ -36,7 +42,7 @@ int main() {
   double* d_sink;
   cudaMalloc(&d_out, 8);
   cudaMalloc(&d_sink, 8);
-  const int smem = (27 * 2 * N + 27 * Rec<N>::STRIDE) * 8;
+  const int smem = (27 * 2 * (N + 2) + 27 * Rec<N>::STRIDE) * 8;
   cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int warps : {1, 3, 9}) {
     k_lu<<<1, 32 * warps, smem>>>(200, d_out, d_sink);
