@@ -55,7 +55,7 @@ def test_with_params_keeps_count():
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "chunkode_b200.h")).read()
-    return sorted(set(re.findall(r"\b(cko_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(cko_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_python_exports():
