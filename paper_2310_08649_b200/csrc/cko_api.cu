@@ -429,13 +429,14 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
   const bool v2 = !pcr && c->kernel_gen >= 2 && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const bool p2 = pcr && c->kernel_gen >= 2 && launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   int G;
   Slab slab;
-  if (v2) {
+  if (v2 || p2) {
     G = nb < c->sms ? nb : c->sms;
     slab.Lmax = (nb + G - 1) / G;
     slab.Pmax = nc_eff * slab.Lmax;
-    slab.doubles = (size_t)slab.Pmax * (n + 1);
+    slab.doubles = (size_t)slab.Pmax * (n + 1) + (p2 ? (size_t)slab.Pmax * pcr2_ws_bound(n) : 0);
     slab.ints = 0;
     CUDA_TRY(c->slab.ensure(sizeof(double) * slab.doubles * G));
     slab.base = c->slab.as<double>();
@@ -489,11 +490,13 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   c->mark(0);
   if (v2)
     CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
+  else if (p2)
+    CUDA_TRY(launch_forward_pcr2(m->dm.kind, n, &a, c->stream));
   else
     CUDA_TRY(launch_forward(a, c->stream));
   c->mark(1);
   c->last_launches = 1;
-  c->last_gen = v2 ? 2 : 1;
+  c->last_gen = (v2 || p2) ? 2 : 1;
   int info[4];
   unsigned long long key;
   CUDA_TRY(cudaMemcpyAsync(info, c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
@@ -577,10 +580,18 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
   const bool v2 = !pcr && c->kernel_gen >= 2 && launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
-  const int G = v2 ? (nb < c->sms ? nb : c->sms) : (nb < 2 * c->sms ? nb : 2 * c->sms);
+  const bool p2 = pcr && c->kernel_gen >= 2 && launch_adjoint_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const int G = (v2 || p2) ? (nb < c->sms ? nb : c->sms) : (nb < 2 * c->sms ? nb : 2 * c->sms);
   Slab slab{};
-  if (!v2)
+  if (p2) {
+    slab.Lmax = (nb + G - 1) / G;
+    slab.Pmax = nc_eff * slab.Lmax;
+    slab.doubles = (size_t)slab.Pmax * pcr2_ws_bound(n);
+    CUDA_TRY(c->slab.ensure(sizeof(double) * slab.doubles * G));
+    slab.base = c->slab.as<double>();
+  } else if (!v2) {
     if (cko_status s = prepare_slab(c, G, nb, nc_eff, n, pcr, slab, err)) return s;
+  }
   const size_t row = (size_t)nb * n;
   CUDA_TRY(c->lambda.ensure(sizeof(double) * row));
   CUDA_TRY(c->wq.ensure(sizeof(double) * row * (nt + 1)));
@@ -595,7 +606,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(c->grad.ensure(sizeof(double) * np));
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
   c->last_launches = 3;
-  c->last_gen = v2 ? 2 : 1;
+  c->last_gen = (v2 || p2) ? 2 : 1;
   c->mark(6);
   if (loss_kind == CKO_LOSS_FROBENIUS) {
     CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
@@ -623,6 +634,8 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   c->mark(2);
   if (v2)
     CUDA_TRY(launch_adjoint_v2(m->dm.kind, n, &a, c->stream));
+  else if (p2)
+    CUDA_TRY(launch_adjoint_pcr2(m->dm.kind, n, &a, c->stream));
   else
     CUDA_TRY(launch_adjoint(a, c->stream));
   c->mark(3);

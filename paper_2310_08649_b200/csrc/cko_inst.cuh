@@ -2,6 +2,7 @@
 #pragma once
 #include "cko_impl.cuh"
 #include "cko_v2.cuh"
+#include "cko_pcr2.cuh"
 
 #define CKO_INSTANTIATE(NAME, MD)                                                                      \
   namespace cko {                                                                                     \

@@ -17,3 +17,19 @@ cudaError_t adj2_run_constant(int n, const AdjLaunch* a, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 }  // namespace cko
+namespace cko {
+cudaError_t fwdp_run_constant(int n, const FwdLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 1: return v2::fwd_pcr2_launch<v2::ConstantRateS>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+cudaError_t adjp_run_constant(int n, const AdjLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 1: return v2::adj_pcr2_launch<v2::ConstantRateS>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+}  // namespace cko

@@ -19,3 +19,19 @@ cudaError_t adj2_run_mds(int n, const AdjLaunch* a, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 }  // namespace cko
+namespace cko {
+cudaError_t fwdp_run_mds(int n, const FwdLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 4: return v2::fwd_pcr2_launch<v2::MdsS<2>>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+cudaError_t adjp_run_mds(int n, const AdjLaunch* a, cudaStream_t st) {
+  switch (n) {
+    case 4: return v2::adj_pcr2_launch<v2::MdsS<2>>(a, st);
+  }
+  (void)a, (void)st;
+  return cudaErrorNotSupported;
+}
+}  // namespace cko

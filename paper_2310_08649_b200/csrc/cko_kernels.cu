@@ -197,6 +197,18 @@ cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t 
 #undef CALL
 }
 
+cudaError_t launch_forward_pcr2(int kind, int n, const FwdLaunch* a, cudaStream_t st) {
+#define CALL(N) fwdp_run_##N(n, a, st)
+  CKO_SWITCH(kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_adjoint_pcr2(int kind, int n, const AdjLaunch* a, cudaStream_t st) {
+#define CALL(N) adjp_run_##N(n, a, st)
+  CKO_SWITCH(kind, CALL)
+#undef CALL
+}
+
 cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st) {
   solve_kernel<<<a.grid, a.threads, 0, st>>>(a);
   return cudaGetLastError();

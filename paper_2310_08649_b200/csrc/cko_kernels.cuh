@@ -84,6 +84,11 @@ cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st);
 // slab of Pmax * (n + 1) doubles per CTA (residual rows + point norms).
 cudaError_t launch_forward_v2(int kind, int n, const FwdLaunch* a, cudaStream_t st);
 cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t st);
+// v2 PCR / hybrid kernels for small blocks (cko_pcr2.cuh), one CTA per SM.
+// Slab per CTA: Pmax (n + 1) + Pmax * pcr2_ws_bound(n) doubles.
+cudaError_t launch_forward_pcr2(int kind, int n, const FwdLaunch* a, cudaStream_t st);
+cudaError_t launch_adjoint_pcr2(int kind, int n, const AdjLaunch* a, cudaStream_t st);
+inline int pcr2_ws_bound(int n) { return 3 * n * n + 5 * n + 20; }
 // L = sqrt(sum_{m>=1} y^2) into *loss (device); scratch >= 1025 doubles. With a
 // group (world > 1) the sum of squares is summed over ranks first.
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,

@@ -771,6 +771,8 @@ cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
 // instantiation (the v1 kernels then run).
 #define CKO_V2_DECLARE(NAME)                                                    \
   cudaError_t fwd2_run_##NAME(int n, const FwdLaunch* a, cudaStream_t st);      \
-  cudaError_t adj2_run_##NAME(int n, const AdjLaunch* a, cudaStream_t st);
+  cudaError_t adj2_run_##NAME(int n, const AdjLaunch* a, cudaStream_t st);      \
+  cudaError_t fwdp_run_##NAME(int n, const FwdLaunch* a, cudaStream_t st);      \
+  cudaError_t adjp_run_##NAME(int n, const AdjLaunch* a, cudaStream_t st);
 
 }  // namespace cko

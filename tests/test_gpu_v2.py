@@ -33,16 +33,36 @@ def _check(got, want):
     assert rel_max(got.gradient, want.grad) <= TOL
 
 
+PCR2_KINDS = {"lin3", "mds_small", "chaboche", "scalar", "constant"}  # block size <= 8
+
+
 @pytest.mark.parametrize("name", ALL_CASES)
 @pytest.mark.parametrize("gen", [1, 2])
-def test_generation_parity(port, name, gen):
+@pytest.mark.parametrize("solver", [(0, 1), (1, 1), (2, 1), (2, 0), (2, 3)])
+def test_generation_parity(port, name, gen, solver):
     m, y0, t, nc = case(name)
-    want = port.gradient(m, y0, t, nc, solver=(0, 1))
+    want = port.gradient(m, y0, t, nc, solver=solver)
     ctx = _ctx(gen)
-    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, ctx=ctx)
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, solver=api.SolverChoice(*solver), ctx=ctx)
     _check(got, want)
-    expect = 2 if (gen == 2 and name in V2_KINDS) else 1
+    kinds = V2_KINDS if solver[0] == 0 else PCR2_KINDS
+    expect = 2 if (gen == 2 and name in kinds) else 1
     assert ctx.kernel_generation_used() == expect
+
+
+@pytest.mark.parametrize("nc", [1, 2, 3, 7, 16, 100, 256, 1000])
+@pytest.mark.parametrize("solver", [(1, 1), (2, 2)])
+def test_pcr2_chaboche_chunks(port, nc, solver):
+    """Sparse-batch C3 shape (reduced): PCR / hybrid over ragged partitions, chunks in shared memory (<= 256
+    rows) and in the global workspace (1000 rows)."""
+    m = chaboche_plastic(3, 3)
+    y0 = np.zeros((3, 5))
+    t = uniform_times(1000, 3, 0.5)
+    want = port.gradient(m, y0, t, nc, solver=solver)
+    ctx = _ctx(2)
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, solver=api.SolverChoice(*solver), ctx=ctx)
+    assert ctx.kernel_generation_used() == 2
+    _check(got, want)
 
 
 @pytest.mark.parametrize("nb", [1, 7, 148, 149, 300, 1500])
