@@ -46,13 +46,14 @@ def parse():
     ap.add_argument("--nt", type=int, default=10000)
     ap.add_argument("--n-unit", type=int, default=10)
     ap.add_argument("--t-max", type=float, default=0.01)
-    ap.add_argument("--n-chunk", type=int, default=16)
-    ap.add_argument("--solver", default="pcr", choices=["thomas", "pcr", "hybrid"])
+    ap.add_argument("--n-chunk", type=int, default=100)
+    ap.add_argument("--solver", default="thomas", choices=["thomas", "pcr", "hybrid"])
     ap.add_argument("--n-switch", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=32)
     ap.add_argument("--quiet-clocks", action="store_true", help="skip nvidia-smi sampling (profiler runs)")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 chunked-PCR vs sequential side measurement")
     return ap.parse_args()
 
 
@@ -139,6 +140,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def load_traffic(kernel, args):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture of this configuration
+    (profiles/traffic.json, written from `ncu --set full` by scripts/ncu_traffic.py), else None."""
+    try:
+        tab = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    key = f"{kernel}:{args.solver}:{args.n_chunk}:{args.nb}:{args.nt}"
+    return tab.get(key)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -220,6 +232,34 @@ def cpu_baseline_single(args):
     return {"value": args.nb * nt_s / sec, "unit": "series*steps/s", "cores": 1, "kind": kind,
             "sample": f"nb={args.nb} lanes x first {nt_s} steps (same dt), single thread, forward+adjoint, "
                       f"{sec:.1f} s"}
+
+
+def c3_pcr_vs_sequential(ctx, reps=2):
+    """North-star side target: stiff Chaboche (eps_a x10), sparse batch nb=50, nt=20000,
+    forward + adjoint through the public API on this GPU: chunked PCR (n_chunk=256) against sequential
+    stepping (n_chunk=1). Device-resident host calls, wall clock around synchronous calls."""
+    import paper_2310_08649_b200 as P
+    from paper_2310_08649_b200 import api
+    nb, nt, nu = 50, 20000, 3
+    m = P.build_chaboche(nu, nb)
+    p = m.params.copy()
+    p[6 + 2 * nu:6 + 2 * nu + nb] *= 10.0
+    m = m.with_params(p)
+    grid = api.TimeGrid.uniform(nt, nb, 10.0)
+    y0 = np.zeros((nb, m.state_size))
+    out = {}
+    for name, kind, nc in (("sequential", 0, 1), ("pcr", 1, 256)):
+        sv = api.SolverChoice(kind, 1)
+        api.gradient_adjoint(m, y0, grid, nc, solver=sv, ctx=ctx)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = api.gradient_adjoint(m, y0, grid, nc, solver=sv, ctx=ctx)
+        out[name] = {"n_chunk": nc, "seconds": (time.perf_counter() - t0) / reps,
+                     "newton_iterations": r.trajectory.work.newton_iterations,
+                     "kernel_generation": ctx.kernel_generation_used()}
+    out["speedup_pcr_over_sequential"] = out["sequential"]["seconds"] / out["pcr"]["seconds"]
+    out["workload"] = "C3 Chaboche n_unit=3 (n=5), eps_a x10, nb=50, nt=20000, t_max=10, forward+adjoint"
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -381,6 +421,16 @@ def main():
         "gpu_launches": rec["launches"],
         "e2e": e2e,
     }
+    line["kernel_generation"] = L.cko_ctx_kernel_generation_used(ctx.h)
+    traffic = load_traffic(dom, args)
+    if traffic is not None:
+        line["roofline"]["traffic"] = traffic["bytes_per_launch"]
+        line["roofline"]["traffic_source"] = traffic["source"]
+    if world == 1 and not args.no_c3:
+        try:
+            line["c3_pcr_vs_sequential"] = c3_pcr_vs_sequential(api.Context(local))
+        except Exception as ex:
+            line["c3_pcr_vs_sequential"] = {"error": str(ex)[:200]}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_single(args)
