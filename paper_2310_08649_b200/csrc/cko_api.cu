@@ -602,7 +602,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(cudaMemsetAsync(c->status.p, 0, sizeof(unsigned), c->stream));
   if (c->grp.world > 1 && np > c->grp.red_cap)
     return fail(err, CKO_COMM, "parameter count %d exceeds the group reduce buffer (%d)", np, c->grp.red_cap);
-  CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm)));
+  CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm, nb, nt)));
   CUDA_TRY(c->grad.ensure(sizeof(double) * np));
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
   c->last_launches = 3;

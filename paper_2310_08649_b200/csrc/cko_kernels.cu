@@ -147,7 +147,15 @@ __global__ void vjp_final_kernel(const double* part, int nblk, int np, double* g
 }
 
 
-size_t vjp_scratch_doubles(const DevModel& m) { return (size_t)kVjpBlocks * m.np; }
+bool vjp_needs_outer(const DevModel& m) {
+  int lo, hi;
+  lane_segment(m, lo, hi);
+  return m.kind == 5 && m.np - (hi - lo) > 1024;
+}
+
+size_t vjp_scratch_doubles(const DevModel& m, int nb, int nt) {
+  return vjp_needs_outer(m) ? node_vjp_scratch_doubles(m, nb, nt) : (size_t)kVjpBlocks * m.np;
+}
 
 #define CKO_SWITCH(KIND, CALL)            \
   switch (KIND) {                         \
@@ -223,6 +231,7 @@ static cudaError_t vjp_dispatch(const DevModel& m, const double* states, const d
 
 cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
                        int nt, double* scratch, double* grad, cudaStream_t st) {
+  if (vjp_needs_outer(m)) return launch_node_vjp(m, states, times, wq, nb, nt, scratch, grad, st);
   cudaError_t e = vjp_dispatch(m, states, times, wq, nb, nt, scratch, st);
   if (e != cudaSuccess) return e;
   vjp_final_kernel<<<(m.np + 255) / 256, 256, 0, st>>>(scratch, kVjpBlocks, m.np, grad);

@@ -97,7 +97,13 @@ cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, 
 cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cnt, unsigned* status,
                              cudaStream_t st);
 // grad (device, np) = sum over (m >= 1, b) of w . dh/dp; scratch sized by vjp_scratch_doubles.
-size_t vjp_scratch_doubles(const DevModel& m);
+size_t vjp_scratch_doubles(const DevModel& m, int nb, int nt);
+// Wide neural ODE (parameter count beyond the per-thread accumulators): the
+// VJP as split-K outer products (cko_node_vjp.cu).
+bool vjp_needs_outer(const DevModel& m);
+size_t node_vjp_scratch_doubles(const DevModel& m, int nb, int nt);
+cudaError_t launch_node_vjp(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
+                            int nt, double* scratch, double* grad, cudaStream_t st);
 cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times,
                        const double* wq, int nb, int nt, double* scratch, double* grad,
                        cudaStream_t st);

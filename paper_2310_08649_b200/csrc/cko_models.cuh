@@ -279,7 +279,7 @@ struct MChaboche {
 // version here keeps its activations in a per-thread scratch of
 // NODE_SCRATCH doubles (small widths); the wide case runs the batched-GEMM
 // kernels in cko_node_wide.cuh.
-constexpr int NODE_MAX_W = 24;
+constexpr int NODE_MAX_W = 128;
 constexpr int NODE_MAX_N = 16;
 
 struct MNode {
@@ -317,26 +317,23 @@ struct MNode {
     forward(m, t, yl, b, z0, z1, z2, o);
     for (int i = 0; i < m.n; ++i) out[i] = o[i];
   }
+  // J = diag(1 - o^2) W3 diag(1 - z2^2) W2 diag(1 - z1^2) W1[:, :n], one
+  // column at a time so only two width-W vectors are live (models_node.cpp:69-107).
   template <class Y, class J>
   __device__ static void jacobian(const DevModel& m, double t, const Y& y, J& jac, int b) {
     const int n = m.n, W = m.W, w0 = n + 1;
     double yl[NODE_MAX_N], z0[NODE_MAX_N + 1], z1[NODE_MAX_W], z2[NODE_MAX_W], o[NODE_MAX_N];
-    double M1[NODE_MAX_W * NODE_MAX_N];
     for (int i = 0; i < n; ++i) yl[i] = y[i];
     forward(m, t, yl, b, z0, z1, z2, o);
     const double* W1 = m.p;
     const double* W2 = W1 + W * w0 + W;
     const double* W3 = W2 + W * W + W;
-    for (int i = 0; i < W; ++i) {
-      const double g = 1.0 - z1[i] * z1[i];
-      for (int j = 0; j < n; ++j) M1[i * n + j] = g * W1[i * w0 + j];
-    }
-    // M2 = diag(1 - z2^2) W2 M1, then J = diag(1 - o^2) W3 M2, one column at a time
     for (int j = 0; j < n; ++j) {
-      double m2[NODE_MAX_W];
+      double m1[NODE_MAX_W], m2[NODE_MAX_W];
+      for (int i = 0; i < W; ++i) m1[i] = (1.0 - z1[i] * z1[i]) * W1[i * w0 + j];
       for (int i = 0; i < W; ++i) {
         double acc = 0.0;
-        for (int l = 0; l < W; ++l) acc += W2[i * W + l] * M1[l * n + j];
+        for (int l = 0; l < W; ++l) acc += W2[i * W + l] * m1[l];
         m2[i] = (1.0 - z2[i] * z2[i]) * acc;
       }
       for (int i = 0; i < n; ++i) {

@@ -1,0 +1,151 @@
+// cko_node_vjp.cu — parameter VJP of the wide neural ODE (SURVEY §8d C4,
+// W = 128: 18 824 parameters), where the per-thread accumulators of
+// vjp_kernel do not fit. The product sum over every (step, lane) point
+//   g = sum_p w_p . dh/dp(y_p, t_p)        (ode_model.cpp:135-153)
+// factors into outer products of per-point vectors (models_node.cpp:109-151):
+//   d3 = w (1 - o^2), d2 = (W3^T d3)(1 - z2^2), d1 = (W2^T d2)(1 - z1^2)
+//   gW3 = sum d3 z2^T, gW2 = sum d2 z1^T, gW1 = sum d1 z0^T, gb_l = sum d_l.
+// node_vectors_kernel writes the vectors feature-major (x[f * P + p]); the
+// sums are split-K GEMMs (outer_partial_kernel, 32 x 32 output tiles, fixed
+// K slices) followed by a fixed-order reduction, so the result is
+// deterministic.
+#include "cko_kernels.cuh"
+
+namespace cko {
+
+namespace {
+
+constexpr int kOuterKS = 64;  // K slices of the split-K outer products
+constexpr int kTile = 32;
+constexpr int kKc = 64;
+
+__global__ void __launch_bounds__(128) node_vectors_kernel(DevModel m, const double* states, const double* times,
+                                                           const double* wq, int nb, int nt, double* vec, size_t P) {
+  const int n = m.n, W = m.W, w0 = n + 1;
+  const size_t row = (size_t)nb * n;
+  const double* W2 = m.p + W * w0 + W;
+  const double* W3 = W2 + W * W + W;
+  double* Z0 = vec;
+  double* Z1 = Z0 + (size_t)w0 * P;
+  double* Z2 = Z1 + (size_t)W * P;
+  double* D1 = Z2 + (size_t)W * P;
+  double* D2 = D1 + (size_t)W * P;
+  double* D3 = D2 + (size_t)W * P;
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < P; p += (size_t)gridDim.x * blockDim.x) {
+    const int mm = 1 + (int)(p / nb), b = (int)(p % nb);
+    const double* y = states + (size_t)mm * row + (size_t)b * n;
+    const double* w = wq + (size_t)mm * row + (size_t)b * n;
+    double yl[NODE_MAX_N], z0[NODE_MAX_N + 1], z1[NODE_MAX_W], z2[NODE_MAX_W], o[NODE_MAX_N];
+    for (int i = 0; i < n; ++i) yl[i] = y[i];
+    MNode::forward(m, times[(size_t)mm * nb + b], yl, b, z0, z1, z2, o);
+    double d3[NODE_MAX_N], d2[NODE_MAX_W];
+    for (int i = 0; i < n; ++i) d3[i] = w[i] * (1.0 - o[i] * o[i]);
+    for (int i = 0; i < W; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < n; ++l) acc += W3[l * W + i] * d3[l];
+      d2[i] = acc * (1.0 - z2[i] * z2[i]);
+    }
+    for (int i = 0; i < W; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l < W; ++l) acc += W2[l * W + i] * d2[l];
+      D1[(size_t)i * P + p] = acc * (1.0 - z1[i] * z1[i]);
+      D2[(size_t)i * P + p] = d2[i];
+      Z1[(size_t)i * P + p] = z1[i];
+      Z2[(size_t)i * P + p] = z2[i];
+    }
+    for (int i = 0; i < w0; ++i) Z0[(size_t)i * P + p] = z0[i];
+    for (int i = 0; i < n; ++i) D3[(size_t)i * P + p] = d3[i];
+  }
+}
+
+// partial[ks][i][j] = sum_{p in slice ks} A[i][p] * B[j][p] for a 32 x 32 tile
+// (B == nullptr: B[j][p] = 1, the bias column).
+__global__ void __launch_bounds__(256) outer_partial_kernel(const double* A, int R, const double* B, int C, size_t P,
+                                                            double* partial) {
+  __shared__ double sa[kTile][kKc + 1], sb[kTile][kKc + 1];
+  const int tilesC = (C + kTile - 1) / kTile;
+  const int i0 = (blockIdx.x / tilesC) * kTile, j0 = (blockIdx.x % tilesC) * kTile;
+  const int ks = blockIdx.y;
+  const size_t per = (P + gridDim.y - 1) / gridDim.y;
+  const size_t k0 = per * ks, k1 = min(P, k0 + per);
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // thread owns rows ty, ty+16 and cols tx, tx+16
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (size_t kc = k0; kc < k1; kc += kKc) {
+    for (int e = threadIdx.x; e < kTile * kKc; e += blockDim.x) {
+      const int r = e / kKc, q = e % kKc;
+      const size_t k = kc + q;
+      sa[r][q] = (i0 + r < R && k < k1) ? A[(size_t)(i0 + r) * P + k] : 0.0;
+      sb[r][q] = (j0 + r < C && k < k1) ? (B ? B[(size_t)(j0 + r) * P + k] : 1.0) : 0.0;
+    }
+    __syncthreads();
+    for (int q = 0; q < kKc; ++q) {
+      const double a0 = sa[ty][q], a1 = sa[ty + 16][q], b0 = sb[tx][q], b1 = sb[tx + 16][q];
+      acc[0][0] += a0 * b0;
+      acc[0][1] += a0 * b1;
+      acc[1][0] += a1 * b0;
+      acc[1][1] += a1 * b1;
+    }
+    __syncthreads();
+  }
+  double* out = partial + ((size_t)ks * R) * C;
+  for (int u = 0; u < 2; ++u)
+    for (int v = 0; v < 2; ++v) {
+      const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
+      if (i < R && j < C) out[(size_t)i * C + j] = acc[u][v];
+    }
+}
+
+__global__ void outer_reduce_kernel(const double* partial, int KS, int R, int C, double* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < R * C; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int ks = 0; ks < KS; ++ks) s += partial[(size_t)ks * R * C + e];
+    out[e] = s;
+  }
+}
+
+cudaError_t outer_sum(const double* A, int R, const double* B, int C, size_t P, double* partial, double* out,
+                      cudaStream_t st) {
+  const int tiles = ((R + kTile - 1) / kTile) * ((C + kTile - 1) / kTile);
+  outer_partial_kernel<<<dim3(tiles, kOuterKS), 256, 0, st>>>(A, R, B, C, P, partial);
+  outer_reduce_kernel<<<(R * C + 255) / 256, 256, 0, st>>>(partial, kOuterKS, R, C, out);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t node_vjp_scratch_doubles(const DevModel& m, int nb, int nt) {
+  const size_t P = (size_t)nb * nt;
+  const int n = m.n, W = m.W, w0 = n + 1;
+  return P * (size_t)(w0 + 4 * W + n) + (size_t)kOuterKS * W * W;
+}
+
+cudaError_t launch_node_vjp(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
+                            int nt, double* scratch, double* grad, cudaStream_t st) {
+  const size_t P = (size_t)nb * nt;
+  const int n = m.n, W = m.W, w0 = n + 1;
+  double* vec = scratch;
+  double* partial = scratch + P * (size_t)(w0 + 4 * W + n);
+  node_vectors_kernel<<<4 * 148, 128, 0, st>>>(m, states, times, wq, nb, nt, vec, P);
+  const double* Z0 = vec;
+  const double* Z1 = Z0 + (size_t)w0 * P;
+  const double* Z2 = Z1 + (size_t)W * P;
+  const double* D1 = Z2 + (size_t)W * P;
+  const double* D2 = D1 + (size_t)W * P;
+  const double* D3 = D2 + (size_t)W * P;
+  // parameter layout [W1 (W x w0), b1, W2 (W x W), b2, W3 (n x W), b3]
+  double* gW1 = grad;
+  double* gb1 = gW1 + W * w0;
+  double* gW2 = gb1 + W;
+  double* gb2 = gW2 + W * W;
+  double* gW3 = gb2 + W;
+  double* gb3 = gW3 + n * W;
+  cudaError_t e;
+  if ((e = outer_sum(D1, W, Z0, w0, P, partial, gW1, st)) != cudaSuccess) return e;
+  if ((e = outer_sum(D1, W, nullptr, 1, P, partial, gb1, st)) != cudaSuccess) return e;
+  if ((e = outer_sum(D2, W, Z1, W, P, partial, gW2, st)) != cudaSuccess) return e;
+  if ((e = outer_sum(D2, W, nullptr, 1, P, partial, gb2, st)) != cudaSuccess) return e;
+  if ((e = outer_sum(D3, n, Z2, W, P, partial, gW3, st)) != cudaSuccess) return e;
+  return outer_sum(D3, n, nullptr, 1, P, partial, gb3, st);
+}
+
+}  // namespace cko
