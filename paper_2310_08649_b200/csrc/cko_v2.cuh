@@ -49,7 +49,14 @@ struct GroupLane {
   }
 };
 
-constexpr int kMaxWarps = 10;  // <= 3 warps per SMSP: up to 168 registers per thread
+constexpr int kMaxWarps = 12;  // 3 warps per SMSP: up to 168 registers per thread
+constexpr int kMaxProducers = 9;  // warp 0 consumes alone on SMSP 0 (warps 4, 8 idle)
+
+// producer index of a warp, -1 for the consumer (0) and the idle warps (4, 8)
+__device__ __forceinline__ int producer_of(int warp) {
+  if ((warp & 3) == 0) return -1;
+  return warp - 1 - (warp >> 2);
+}
 constexpr int kMaxSlots = 7;  // named barriers 1..2S must stay below 16
 constexpr int kMaxWs = 3;     // producer warps per slot
 
@@ -413,10 +420,11 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
   const int S = sh.S, Ws = sh.Ws;
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
-  if (warp < S * Ws) {
+  const int pw = producer_of(warp);
+  if (pw >= 0 && pw < S * Ws) {
     // ---- producer: J -> M = I - J dt -> LU for rows k = s, s + S, ...; it
     // also stages r_k and yy_k in the record so the consumer never waits on L2.
-    const int s = warp / Ws, sw = warp % Ws;
+    const int s = pw / Ws, sw = pw % Ws;
     const GroupLane<N> gr(lane);
     const int g = gr.g, gl = gr.gl;
     const int lt = sw * Gm::GPW + g;
@@ -462,7 +470,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       if (tr) tr[k * 8 + 3] = globaltimer_ns();
       bar_arrive(1 + s, nthr);
     }
-  } else if (warp == S * Ws) {
+  } else if (warp == 0) {
     // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, one thread per lane
     const int lt = lane;
     const bool active = lt < LTc;
@@ -591,8 +599,9 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
   const size_t row = (size_t)nb * N;
-  if (warp < S * Ws) {
-    const int s = warp / Ws, sw = warp % Ws;
+  const int pw = producer_of(warp);
+  if (pw >= 0 && pw < S * Ws) {
+    const int s = pw / Ws, sw = pw % Ws;
     const GroupLane<N> gr(lane);
     const int g = gr.g, gl = gr.gl;
     const int lt = sw * Gm::GPW + g;
@@ -648,7 +657,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + s, nthr);
     }
-  } else if (warp == S * Ws) {
+  } else if (warp == 0) {
     const int lt = lane;
     const bool active = lt < LTc;
     const int b = lb0 + t0 + lt;
@@ -693,7 +702,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
   int lb0, L;
   lane_range(a.nb, lb0, L);
   const double Lval = a.loss ? *a.loss : 0.0;
-  const int consumer = threadIdx.x >> 5 == sh.S * sh.Ws;
+  const int consumer = threadIdx.x >> 5 == 0;
   const int lane = threadIdx.x & 31;
   for (int t0 = 0; t0 < L; t0 += sh.LT) {
     const int LTc = min(sh.LT, L - t0);
@@ -730,10 +739,10 @@ inline Shape make_shape(int L) {
   if (Ws > kMaxWs) Ws = kMaxWs;
   if (Ws < 1) Ws = 1;
   sh.Ws = Ws;
-  sh.S = (kMaxWarps - 1) / Ws;  // ring depth: as many slots as the warp budget allows
+  sh.S = kMaxProducers / Ws;  // ring depth: as many slots as the producer warps allow
   if (sh.S > kMaxSlots) sh.S = kMaxSlots;
   sh.LT = Ws * gpw < 32 ? Ws * gpw : 32;  // lanes per tile == records per slot
-  sh.threads = 32 * (sh.S * sh.Ws + 1);
+  sh.threads = 32 * kMaxWarps;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
   smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
   sh.smem_bytes = tot * 8;
