@@ -122,6 +122,31 @@ long long sweeps_of(int c, int kind, int n_switch) {
 
 }  // namespace
 
+// Grow-only pinned host staging for the small device-to-host results of every
+// call (status words, chunk iteration counts, loss, gradient): pinned copies
+// stay asynchronous on the context stream and never wait on other streams.
+struct PinBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
+    release();
+    const size_t want = b < (256u << 10) ? (256u << 10) : 2 * b;
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T>
+  T* as(size_t byte_offset = 0) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p) + byte_offset);
+  }
+};
+
 struct cko_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -131,6 +156,7 @@ struct cko_ctx {
   Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
   Buf h_y0, h_times, h_states, h_dL, h_rhs, h_diag, h_off;  // staging for host-buffer calls
   std::vector<int> iters_host;
+  PinBuf pin;
   // batch sharding
   GroupView grp{};
   // kernel timing (cko_ctx_enable_timing)
@@ -216,6 +242,7 @@ cko_status cko_ctx_destroy(cko_ctx* c) {
                  &c->scratch, &c->lambda, &c->wq, &c->vjp, &c->grad, &c->h_y0, &c->h_times,
                  &c->h_states, &c->h_dL, &c->h_rhs, &c->h_diag, &c->h_off})
     b->release();
+  c->pin.release();
   for (cudaEvent_t& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -499,12 +526,16 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   c->last_gen = (v2 || p2) ? 2 : 1;
   int info[4];
   unsigned long long key;
-  CUDA_TRY(cudaMemcpyAsync(info, c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
-  c->iters_host.resize(n_chunks);
-  CUDA_TRY(cudaMemcpyAsync(c->iters_host.data(), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
+  CUDA_TRY(c->pin.ensure(32 + sizeof(int) * (size_t)n_chunks));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(0), c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(32), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::memcpy(info, c->pin.as<int>(0), sizeof info);
+  key = *c->pin.as<unsigned long long>(16);
+  c->iters_host.assign(c->pin.as<int>(32), c->pin.as<int>(32) + n_chunks);
   if (a.trace) {
     std::vector<unsigned long long> h(tbuf.bytes / sizeof(unsigned long long));
     CUDA_TRY(cudaMemcpy(h.data(), tbuf.p, tbuf.bytes, cudaMemcpyDeviceToHost));
@@ -651,12 +682,19 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   unsigned long long key;
   unsigned gstatus = 0;
   double L = NAN;
-  CUDA_TRY(cudaMemcpyAsync(&gstatus, c->status.p, sizeof gstatus, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(&key, c->key.p, sizeof key, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c->pin.ensure(32 + sizeof(double) * (size_t)np));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned>(0), c->status.p, sizeof gstatus, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(8), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                           c->stream));
   if (loss_kind == CKO_LOSS_FROBENIUS)
-    CUDA_TRY(cudaMemcpyAsync(&L, c->loss.p, sizeof L, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(grad_out, c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(16), c->loss.p, sizeof L, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(32), c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost,
+                           c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  gstatus = *c->pin.as<unsigned>(0);
+  key = *c->pin.as<unsigned long long>(8);
+  if (loss_kind == CKO_LOSS_FROBENIUS) L = *c->pin.as<double>(16);
+  std::memcpy(grad_out, c->pin.as<double>(32), sizeof(double) * np);
   c->last_ms[0] = 0.0;
   c->collect(1, 3);
   if (gstatus) return fail(err, CKO_COMM, "group reduction timed out (peer stalled)");

@@ -5,9 +5,34 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace cko {
+
+// Raise a kernel's dynamic shared-memory limit to 226 KB (227 KB minus the static
+// part) once per
+// process (thread-safe static init). Setting it on every launch would
+// serialise concurrent launches of the same kernel from other streams: the
+// attribute write waits for running instances.
+#define CKO_ALLOW_FULL_SMEM(KERNEL)                                                                    \
+  do {                                                                                                \
+    static const cudaError_t _cko_attr_err = cudaFuncSetAttribute(                                    \
+        (const void*)(KERNEL), cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);              \
+    if (_cko_attr_err != cudaSuccess) return _cko_attr_err;                                           \
+  } while (0)
+
+// Persistent grid-barrier kernels launch cooperatively (every CTA resident).
+// CKO_PLAIN_LAUNCH=1 switches to an ordinary launch: used only by the
+// single-GPU group test, where two ranks' small grids must run concurrently
+// and CUDA does not overlap two cooperative launches (the grids there are a
+// few CTAs, resident either way).
+inline cudaError_t launch_persistent(const void* func, dim3 grid, dim3 block, void** args, size_t smem,
+                                     cudaStream_t st) {
+  const char* plain = std::getenv("CKO_PLAIN_LAUNCH");
+  if (plain && plain[0] == '1') return cudaLaunchKernel(func, grid, block, args, smem, st);
+  return cudaLaunchCooperativeKernel(func, grid, block, args, smem, st);
+}
 
 // Per-CTA workspace slabs are stored component-major / point-minor:
 // element e of point p lives at base[e * stride + p], so consecutive threads

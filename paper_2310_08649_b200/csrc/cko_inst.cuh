@@ -9,7 +9,7 @@
   cudaError_t fwd_run_##NAME(const FwdLaunch& a, cudaStream_t st) {                                   \
     FwdLaunch copy = a;                                                                               \
     void* args[] = {&copy};                                                                           \
-    return cudaLaunchCooperativeKernel((const void*)fwd_kernel<MD>, dim3(a.grid), dim3(a.threads),    \
+    return launch_persistent((const void*)fwd_kernel<MD>, dim3(a.grid), dim3(a.threads),    \
                                        args, 0, st);                                                  \
   }                                                                                                   \
   cudaError_t fwd_occ_##NAME(int threads, int* blocks) {                                              \

@@ -488,12 +488,11 @@ cudaError_t fwd_pcr2_launch(const FwdLaunch* a, cudaStream_t st) {
   const size_t ocs = ((MS::NCONST + 1) / 2) * 2;
   const bool in_smem = (ocs + ws) * 8 <= kPcr2SmemBudget;
   const int smem = (int)((ocs + (in_smem ? ws : 0)) * 8);
-  cudaError_t e = cudaFuncSetAttribute(fwd_pcr2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  CKO_ALLOW_FULL_SMEM(fwd_pcr2_kernel<MS>);
   FwdLaunch copy = *a;
   int flag = in_smem ? 1 : 0;
   void* args[] = {&copy, &flag};
-  return cudaLaunchCooperativeKernel((const void*)fwd_pcr2_kernel<MS>, dim3(a->grid),
+  return launch_persistent((const void*)fwd_pcr2_kernel<MS>, dim3(a->grid),
                                      dim3(pcr2_threads<MS>(c, Lmax)), args, smem, st);
 }
 
@@ -507,8 +506,7 @@ cudaError_t adj_pcr2_launch(const AdjLaunch* a, cudaStream_t st) {
   const size_t olam = ocs + ((Lmax * MS::N + 1) / 2) * 2;
   const bool in_smem = (olam + ws) * 8 <= kPcr2SmemBudget;
   const int smem = (int)((olam + (in_smem ? ws : 0)) * 8);
-  cudaError_t e = cudaFuncSetAttribute(adj_pcr2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  CKO_ALLOW_FULL_SMEM(adj_pcr2_kernel<MS>);
   adj_pcr2_kernel<MS><<<a->grid, pcr2_threads<MS>(c, Lmax), smem, st>>>(*a, in_smem ? 1 : 0);
   return cudaGetLastError();
 }

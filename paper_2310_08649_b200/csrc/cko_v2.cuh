@@ -754,11 +754,10 @@ cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
   if (!a) return cudaSuccess;
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   Shape sh = make_shape<MS>(Lmax);
-  cudaError_t e = cudaFuncSetAttribute(fwd2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes);
-  if (e != cudaSuccess) return e;
+  CKO_ALLOW_FULL_SMEM(fwd2_kernel<MS>);
   FwdLaunch copy = *a;
   void* args[] = {&copy, &sh};
-  return cudaLaunchCooperativeKernel((const void*)fwd2_kernel<MS>, dim3(a->grid), dim3(sh.threads), args,
+  return launch_persistent((const void*)fwd2_kernel<MS>, dim3(a->grid), dim3(sh.threads), args,
                                      sh.smem_bytes, st);
 }
 
@@ -767,8 +766,7 @@ cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
   if (!a) return cudaSuccess;
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   Shape sh = make_shape<MS>(Lmax);
-  cudaError_t e = cudaFuncSetAttribute(adj2_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem_bytes);
-  if (e != cudaSuccess) return e;
+  CKO_ALLOW_FULL_SMEM(adj2_kernel<MS>);
   adj2_kernel<MS><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
   return cudaGetLastError();
 }
