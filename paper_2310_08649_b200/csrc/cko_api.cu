@@ -455,7 +455,9 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   const int n = m->dm.n;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const bool v2 = !pcr && c->kernel_gen >= 2 && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const bool nodep = !pcr && c->kernel_gen >= 2 && node_fast_path(m->dm);
+  const bool v2 = !nodep && !pcr && c->kernel_gen >= 2 &&
+                  launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const bool p2 = pcr && c->kernel_gen >= 2 && launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   int G;
   Slab slab;
@@ -514,6 +516,27 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
     CUDA_TRY(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, c->stream));
     a.trace = tbuf.as<unsigned long long>();
   }
+  int info[4];
+  unsigned long long key;
+  if (nodep) {  // wide neural ODE: DMMA model evaluation, host-driven Newton loop (cko_node.cu)
+    CUDA_TRY(c->scratch.ensure(sizeof(double) * node_scratch_doubles(nb, nc_eff)));
+    CUDA_TRY(c->status.ensure(sizeof(unsigned)));
+    CUDA_TRY(c->pin.ensure(64));
+    std::memset(info, 0, sizeof info);
+    c->iters_host.assign(n_chunks, 0);
+    c->mark(0);
+    CUDA_TRY(node_forward(m->dm, d_states, d_times, d_dy, nb, nt, nc, st->tol_a, st->tol_r, st->max_iter,
+                          c->scratch.as<double>(), c->r0.as<double>(), c->rn.as<double>(), c->status.as<unsigned>(),
+                          c->pin.as<unsigned>(0), c->key.as<unsigned long long>(), c->grp, c->gs.as<GridSync>(),
+                          c->iters_host.data(), info, c->stream));
+    c->mark(1);
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    key = *c->pin.as<unsigned long long>(16);
+    c->last_launches = 1 + 6 * (int)n_chunks;
+    c->last_gen = 2;
+  } else {
   c->mark(0);
   if (v2)
     CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
@@ -524,8 +547,6 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   c->mark(1);
   c->last_launches = 1;
   c->last_gen = (v2 || p2) ? 2 : 1;
-  int info[4];
-  unsigned long long key;
   CUDA_TRY(c->pin.ensure(32 + sizeof(int) * (size_t)n_chunks));
   CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(0), c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
@@ -536,6 +557,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   std::memcpy(info, c->pin.as<int>(0), sizeof info);
   key = *c->pin.as<unsigned long long>(16);
   c->iters_host.assign(c->pin.as<int>(32), c->pin.as<int>(32) + n_chunks);
+  }
   if (a.trace) {
     std::vector<unsigned long long> h(tbuf.bytes / sizeof(unsigned long long));
     CUDA_TRY(cudaMemcpy(h.data(), tbuf.p, tbuf.bytes, cudaMemcpyDeviceToHost));
@@ -610,11 +632,15 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   const int n = m->dm.n, np = m->dm.np;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const bool v2 = !pcr && c->kernel_gen >= 2 && launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const bool nodep = !pcr && c->kernel_gen >= 2 && node_fast_path(m->dm);
+  const bool v2 = !nodep && !pcr && c->kernel_gen >= 2 &&
+                  launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const bool p2 = pcr && c->kernel_gen >= 2 && launch_adjoint_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const int G = (v2 || p2) ? (nb < c->sms ? nb : c->sms) : (nb < 2 * c->sms ? nb : 2 * c->sms);
   Slab slab{};
-  if (p2) {
+  if (nodep) {
+    CUDA_TRY(c->slab.ensure(sizeof(double) * node_scratch_doubles(nb, nc_eff)));
+  } else if (p2) {
     slab.Lmax = (nb + G - 1) / G;
     slab.Pmax = nc_eff * slab.Lmax;
     slab.doubles = (size_t)slab.Pmax * pcr2_ws_bound(n);
@@ -637,7 +663,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(c->grad.ensure(sizeof(double) * np));
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
   c->last_launches = 3;
-  c->last_gen = (v2 || p2) ? 2 : 1;
+  c->last_gen = (nodep || v2 || p2) ? 2 : 1;
   c->mark(6);
   if (loss_kind == CKO_LOSS_FROBENIUS) {
     CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
@@ -663,7 +689,10 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.grid = G;
   a.threads = kThreads;
   c->mark(2);
-  if (v2)
+  if (nodep)
+    CUDA_TRY(node_adjoint(m->dm, d_states, d_times, a.dL, a.loss, nb, nt, nc, c->slab.as<double>(),
+                          c->lambda.as<double>(), c->wq.as<double>(), c->key.as<unsigned long long>(), c->stream));
+  else if (v2)
     CUDA_TRY(launch_adjoint_v2(m->dm.kind, n, &a, c->stream));
   else if (p2)
     CUDA_TRY(launch_adjoint_pcr2(m->dm.kind, n, &a, c->stream));

@@ -84,6 +84,17 @@ cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st);
 // slab of Pmax * (n + 1) doubles per CTA (residual rows + point norms).
 cudaError_t launch_forward_v2(int kind, int n, const FwdLaunch* a, cudaStream_t st);
 cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t st);
+// Wide neural ODE (state 8, width 128) on DMMA tensor cores, host-driven
+// Newton loop (cko_node.cu). Scratch: node_scratch_doubles(nb, min(nc, nt)).
+bool node_fast_path(const DevModel& m);
+size_t node_scratch_doubles(int nb, int c);
+cudaError_t node_forward(const DevModel& m, double* states, const double* times, const double* dy, int nb, int nt,
+                         int nc, double tol_a, double tol_r, int max_iter, double* scratch, double* r0, double* rn,
+                         unsigned* d_flags, unsigned* h_flags, unsigned long long* sing_key, const GroupView& grp,
+                         GridSync* gs, int* iters, int* info, cudaStream_t st);
+cudaError_t node_adjoint(const DevModel& m, const double* states, const double* times, const double* dL,
+                         const double* loss, int nb, int nt, int nc, double* scratch, double* lam, double* wq,
+                         unsigned long long* sing_key, cudaStream_t st);
 // v2 PCR / hybrid kernels for small blocks (cko_pcr2.cuh), one CTA per SM.
 // Slab per CTA: Pmax (n + 1) + Pmax * pcr2_ws_bound(n) doubles.
 cudaError_t launch_forward_pcr2(int kind, int n, const FwdLaunch* a, cudaStream_t st);

@@ -1,0 +1,457 @@
+// cko_node.cu — the wide neural ODE (state 8, hidden width
+// 128) on fp64 tensor cores.
+//
+// Every rate and Jacobian evaluation of the MLP right-hand side
+//   h = tanh(W3 tanh(W2 tanh(W1 [y; s] + b1) + b2) + b3),
+//   J = diag(1 - o^2) W3 diag(1 - z2^2) W2 diag(1 - z1^2) W1[:, :8]
+// (models_node.cpp:37-107) is dominated by W2 (128 x 128) times per-point
+// operands. node_eval_kernel batches 8 points per tile and runs those products
+// as DMMA m8n8k4 (mma.sync f64, SASS DMMA.8x8x4) against one operand matrix
+// [M1 of 8 points (64 columns) | z1 of 8 points (8 columns)]: 72 columns,
+// 9 tile columns, 32 k-steps.
+//
+// The Newton loop around it runs from the host (one launch per phase, the
+// all-lanes predicate read back through pinned memory): node_residual_kernel
+// (integrate.cpp:64-95), node_factor_kernel (thread per point: M = I - J dt,
+// LU with the reference's pivot rule) and node_thomas_kernel (thread per lane:
+// substitution, iterate update). The adjoint uses the same pieces on
+// (I - J dt)^T (adjoint.cpp:49-127). Arithmetic outside the DMMA products
+// follows the reference; the products accumulate in tensor-core order.
+#include <cmath>
+#include <cstring>
+
+#include "cko_kernels.cuh"
+#include "cko_lu_thread.cuh"
+
+namespace cko {
+namespace node {
+
+constexpr int N = 8, W = 128, W0 = N + 1;
+constexpr int TP = 8;                 // points per tile
+constexpr int BC = TP * N + TP;       // operand columns: M1 (64) | z1 (8)
+constexpr int kEvalThreads = 256;
+
+struct Views {
+  const double *W1, *b1, *W2, *b2, *W3, *b3;
+  __device__ explicit Views(const double* p) {
+    W1 = p;
+    b1 = W1 + W * W0;
+    W2 = b1 + W;
+    b2 = W2 + W * W;
+    W3 = b2 + W;
+    b3 = W3 + N * W;
+  }
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Points are (k, b) pairs of a chunk, p = k * nb + b, state rows at
+// states[(row0 + k) * nb * N + b * N], times t[(row0 + k) * nb + b]. H (P, N)
+// receives h, J (P, N, N) the Jacobian (when want_j).
+constexpr int kEvalSmem = (2 * W * BC + TP * W0 + TP * N) * 8;  // operand, products, z0, 1 - o^2
+
+// Point p = k * nb + b sits on trajectory row row0 + dir * k (dir = -1: the
+// descending rows of a reversed adjoint chunk).
+__global__ void __launch_bounds__(kEvalThreads) node_eval_kernel(DevModel m, const double* states,
+                                                                 const double* times, int row0, int dir, int nb,
+                                                                 int P, double* H, double* J, int want_j) {
+  extern __shared__ __align__(16) double smem[];
+  double* sB = smem;               // operand  (W x 72) = 72 KB
+  double* sX = sB + W * BC;        // products (W x 72) = 72 KB
+  double (*sz0)[W0] = reinterpret_cast<double (*)[W0]>(sX + W * BC);
+  double (*sg3)[N] = reinterpret_cast<double (*)[N]>(sX + W * BC + TP * W0);
+  const Views v(m.p);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = (P + TP - 1) / TP;
+  const size_t row = (size_t)nb * N;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int p0 = tile * TP;
+    // z0 = [y; sin(2 pi t / T_b)]
+    for (int e = tid; e < TP * W0; e += blockDim.x) {
+      const int q = e / W0, i = e % W0, p = min(p0 + q, P - 1);
+      const int k = p / nb, b = p % nb, rw = row0 + dir * k;
+      if (i < N)
+        sz0[q][i] = states[(size_t)rw * row + (size_t)b * N + i];
+      else
+        sz0[q][i] = sin(CKO_TWO_PI * times[(size_t)rw * nb + b] / m.periods[m.off + b]);
+    }
+    __syncthreads();
+    // z1 = tanh(W1 z0 + b1); operand columns: M1 = (1 - z1^2) W1[:, :8] per point, then z1
+    for (int e = tid; e < TP * W; e += blockDim.x) {
+      const int q = e / W, i = e % W;
+      double acc = v.b1[i];
+      for (int j = 0; j < W0; ++j) acc += v.W1[i * W0 + j] * sz0[q][j];
+      const double z1 = tanh(acc), g1 = 1.0 - z1 * z1;
+      double* brow = sB + i * BC;
+      for (int j = 0; j < N; ++j) brow[q * N + j] = g1 * v.W1[i * W0 + j];
+      brow[TP * N + q] = z1;
+    }
+    __syncthreads();
+    // X = W2 [M1 | z1] on the tensor cores: warp w owns rows 16w..16w+15 (two 8-row tiles)
+    {
+      double acc[2][BC / 8][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < BC / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const int r0 = warp * 16;
+      for (int k = 0; k < W; k += 4) {
+        const double a0 = __ldg(v.W2 + (r0 + lane / 4) * W + k + lane % 4);
+        const double a1 = __ldg(v.W2 + (r0 + 8 + lane / 4) * W + k + lane % 4);
+#pragma unroll
+        for (int j = 0; j < BC / 8; ++j) {
+          const double bv = sB[(k + lane % 4) * BC + 8 * j + lane / 4];
+          dmma(acc[0][j][0], acc[0][j][1], a0, bv);
+          dmma(acc[1][j][0], acc[1][j][1], a1, bv);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < BC / 8; ++j) {
+          double* out = sX + (r0 + 8 * i + lane / 4) * BC + 8 * j + 2 * (lane % 4);
+          out[0] = acc[i][j][0];
+          out[1] = acc[i][j][1];
+        }
+    }
+    __syncthreads();
+    // z2 = tanh(a2 + b2); M2 = (1 - z2^2) X in place; z2 kept in the z1 columns
+    for (int e = tid; e < TP * W; e += blockDim.x) {
+      const int q = e / W, i = e % W;
+      double* xrow = sX + i * BC;
+      const double z2 = tanh(xrow[TP * N + q] + v.b2[i]), g2 = 1.0 - z2 * z2;
+      xrow[TP * N + q] = z2;
+      for (int j = 0; j < N; ++j) xrow[q * N + j] *= g2;
+    }
+    __syncthreads();
+    // o = tanh(W3 z2 + b3), h = o
+    for (int e = tid; e < TP * N; e += blockDim.x) {
+      const int q = e / N, i = e % N, p = p0 + q;
+      double acc = v.b3[i];
+      for (int l = 0; l < W; ++l) acc += v.W3[i * W + l] * sX[l * BC + TP * N + q];
+      const double o = tanh(acc);
+      sg3[q][i] = 1.0 - o * o;
+      if (p < P) H[(size_t)p * N + i] = o;
+    }
+    if (want_j) {
+      __syncthreads();
+      // J = diag(g3) W3 M2
+      for (int e = tid; e < TP * N * N; e += blockDim.x) {
+        const int q = e / (N * N), i = (e / N) % N, j = e % N, p = p0 + q;
+        double acc = 0.0;
+        for (int l = 0; l < W; ++l) acc += v.W3[i * W + l] * sX[l * BC + q * N + j];
+        if (p < P) J[(size_t)p * N * N + i * N + j] = sg3[q][i] * acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Residual of the chunk's points + lane norms + predicate flags (integrate.cpp:64-95, 176-188).
+__global__ void node_residual_kernel(const double* states, const double* times, const double* H, int step, int c,
+                                     int nb, double* R, double* r0, double* rn, int first, double tol_a,
+                                     double tol_r, unsigned* flags) {
+  const size_t row = (size_t)nb * N;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < c; ++k) {
+      const int p = k * nb + b;
+      const double t = times[(size_t)(step + 1 + k) * nb + b];
+      const double dt = t - times[(size_t)(step + k) * nb + b];
+      const double* y = states + (size_t)(step + 1 + k) * row + (size_t)b * N;
+      const double* ym = states + (size_t)(step + k) * row + (size_t)b * N;
+      double s = 0.0;
+      for (int i = 0; i < N; ++i) {
+        const double vv = xsub(xsub(y[i], ym[i]), xmul(H[(size_t)p * N + i], dt));
+        R[(size_t)p * N + i] = vv;
+        s = xadd(s, xmul(vv, vv));
+      }
+      acc = xadd(acc, s);
+    }
+    const double nrm = sqrt(acc);
+    double base = nrm;
+    if (first)
+      r0[b] = nrm;
+    else
+      base = r0[b];
+    rn[b] = nrm;
+    unsigned f = 0;
+    if (!isfinite(nrm)) f |= FLAG_NON_FINITE;
+    if (!(nrm <= tol_a || nrm <= xmul(tol_r, base))) f |= FLAG_NOT_CONVERGED;
+    if (f) atomicOr(flags, f);
+  }
+}
+
+constexpr int kRec = N * N + N + 6;  // LU | 1/U_ii | perm (N + 1 ints) — 16-byte aligned stride
+
+// Thread per point: assemble M (forward: I - J dt; adjoint: (I - J dt)^T and the rhs
+// dL + dt J^T lambda) and factor it (lu_factor_block rule).
+__global__ void node_factor_kernel(const double* J, const double* times, int step_or_hi, int c, int nb,
+                                   int adjoint, double* recs, unsigned long long* sing_key, unsigned long long ord,
+                                   int nc) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c * nb; p += gridDim.x * blockDim.x) {
+    const int k = p / nb, b = p % nb;
+    const int m = adjoint ? step_or_hi - k : step_or_hi + 1 + k;
+    const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
+    const double* Jp = J + (size_t)p * N * N;
+    double* rec = recs + (size_t)p * kRec;
+    double mx = 0.0;
+    auto build = [&]() {
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          double vv;
+          if (adjoint)
+            vv = (i == j) ? 1.0 - dt * Jp[j * N + i] : -dt * Jp[j * N + i];
+          else
+            vv = (i == j) ? xadd(xmul(-dt, Jp[i * N + j]), 1.0) : xmul(-dt, Jp[i * N + j]);
+          rec[i * N + j] = vv;
+          mx = fmax(mx, fabs(vv));
+        }
+    };
+    build();
+    bool viol;
+    bool ok = lt::lu_thread_nopiv<N>(rec, rec + N * N, 1e-14 * mx, viol);
+    int* perm = reinterpret_cast<int*>(rec + N * N + N);
+    if (viol) {
+      build();
+      ok = lt::lu_thread_pivot<N>(rec, rec + N * N, perm, 1e-14 * mx);
+      perm[N] = 0;
+    } else {
+      for (int i = 0; i < N; ++i) perm[i] = i;
+      perm[N] = 1;
+    }
+    if (!ok)
+      atomicMin(sing_key, adjoint ? ord * (unsigned long long)nc * nb + (unsigned long long)k * nb + b
+                                  : (unsigned long long)k * nb + b);
+  }
+}
+
+__device__ inline void rec_solve(const double* rec, double (&v)[N]) {
+  const int* perm = reinterpret_cast<const int*>(rec + N * N + N);
+  double y[N];
+  if (perm[N]) {
+    for (int i = 0; i < N; ++i) y[i] = v[i];
+  } else {
+    for (int i = 0; i < N; ++i) y[i] = v[perm[i]];
+  }
+  for (int i = 1; i < N; ++i) {
+    double s = y[i];
+    for (int j = 0; j < i; ++j) s -= rec[i * N + j] * y[j];
+    y[i] = s;
+  }
+  for (int i = N - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int j = i + 1; j < N; ++j) s -= rec[i * N + j] * y[j];
+    y[i] = s * rec[N * N + i];
+  }
+  for (int i = 0; i < N; ++i) v[i] = y[i];
+}
+
+// Thread per lane: forward substitution x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k.
+__global__ void node_thomas_fwd_kernel(double* states, const double* R, const double* recs, int step, int c,
+                                       int nb) {
+  const size_t row = (size_t)nb * N;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    double x[N];
+    for (int i = 0; i < N; ++i) x[i] = 0.0;
+    for (int k = 0; k < c; ++k) {
+      const int p = k * nb + b;
+      double v[N];
+      for (int i = 0; i < N; ++i) v[i] = R[(size_t)p * N + i] + x[i];
+      rec_solve(recs + (size_t)p * kRec, v);
+      double* yy = states + (size_t)(step + 1 + k) * row + (size_t)b * N;
+      for (int i = 0; i < N; ++i) {
+        x[i] = v[i];
+        yy[i] -= v[i];
+      }
+    }
+  }
+}
+
+// Adjoint rhs of a reversed chunk: rhs_r = dL_m + dt J_m^T lambda (adjoint.cpp:64-72).
+__global__ void node_adj_rhs_kernel(const double* states, const double* times, const double* J, const double* dL,
+                                    const double* loss, const double* lam, int step_hi, int c, int nb, double* R) {
+  const size_t row = (size_t)nb * N;
+  const double Lval = loss ? *loss : 0.0;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c * nb; p += gridDim.x * blockDim.x) {
+    const int r = p / nb, b = p % nb, m = step_hi - r;
+    const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
+    const double* Jp = J + (size_t)p * N * N;
+    const double* lb = lam + (size_t)b * N;
+    const double* y = states + (size_t)m * row + (size_t)b * N;
+    double tmp[N];
+    for (int i = 0; i < N; ++i) tmp[i] = 0.0;
+    for (int j = 0; j < N; ++j)
+      for (int i = 0; i < N; ++i) tmp[i] += Jp[j * N + i] * lb[j];
+    for (int i = 0; i < N; ++i) {
+      const double dl = dL ? dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? y[i] / Lval : 0.0);
+      R[(size_t)p * N + i] = dl + dt * tmp[i];
+    }
+  }
+}
+
+// Thread per lane: delta_r = M_r^{-1}(rhs_r + delta_{r-1}), w_m = (lambda + delta_r) dt, lambda += delta_{c-1}.
+__global__ void node_thomas_adj_kernel(const double* R, const double* recs, const double* times, int step_hi,
+                                       int c, int nb, double* lam, double* wq) {
+  const size_t row = (size_t)nb * N;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    double d[N], lc[N];
+    for (int i = 0; i < N; ++i) d[i] = 0.0, lc[i] = lam[(size_t)b * N + i];
+    for (int r = 0; r < c; ++r) {
+      const int p = r * nb + b, m = step_hi - r;
+      const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
+      for (int i = 0; i < N; ++i) d[i] = R[(size_t)p * N + i] + d[i];
+      rec_solve(recs + (size_t)p * kRec, d);
+      double* w = wq + (size_t)m * row + (size_t)b * N;
+      for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
+    }
+    for (int i = 0; i < N; ++i) lam[(size_t)b * N + i] = lc[i] + d[i];
+  }
+}
+
+__global__ void node_init_chunk_kernel(double* states, const double* dy, int step, int c, int nb) {
+  const size_t row = (size_t)nb * N;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)c * row;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / row);
+    const size_t off = e % row;
+    states[(size_t)(step + 1 + k) * row + off] =
+        states[(size_t)step * row + off] + (dy ? dy[(size_t)k * row + off] : 0.0);
+  }
+}
+
+// One-thread exchange of the predicate flags with the group (same generation
+// counter as the grid barriers).
+__global__ void node_group_flags_kernel(GroupView g, GridSync* gs, unsigned* flags, uint64_t budget_ns) {
+  if (threadIdx.x == 0 && g.world > 1) {
+    gs->ext_gen += 1;
+    *flags = group_exchange(g, gs->ext_gen, *flags, globaltimer_ns() + budget_ns);
+  }
+}
+
+inline int blocks_for(size_t work, int threads) {
+  size_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > 148 * 8) b = 148 * 8;
+  return (int)b;
+}
+
+}  // namespace node
+
+bool node_fast_path(const DevModel& m) { return m.kind == 5 && m.n == node::N && m.W == node::W; }
+
+size_t node_scratch_doubles(int nb, int c) {
+  const size_t P = (size_t)nb * c;
+  return P * (node::N + node::N * node::N + node::N + node::kRec) + 8;
+}
+
+cudaError_t node_eval(const DevModel& m, const double* states, const double* times, int row0, int dir, int nb,
+                      int P, double* H, double* J, bool want_j, cudaStream_t st) {
+  static const cudaError_t attr = cudaFuncSetAttribute((const void*)node::node_eval_kernel,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, node::kEvalSmem);
+  if (attr != cudaSuccess) return attr;
+  const int tiles = (P + node::TP - 1) / node::TP;
+  node::node_eval_kernel<<<tiles < 148 ? tiles : 148, node::kEvalThreads, node::kEvalSmem, st>>>(
+      m, states, times, row0, dir, nb, P, H, J, want_j ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// Host-driven Newton integration for the wide neural ODE (Thomas solver).
+// Returns 0 ok, 1 singular (key), 2 divergence (info), 4 group timeout.
+cudaError_t node_forward(const DevModel& m, double* states, const double* times, const double* dy, int nb, int nt,
+                         int nc, double tol_a, double tol_r, int max_iter, double* scratch, double* r0, double* rn,
+                         unsigned* d_flags, unsigned* h_flags, unsigned long long* sing_key, const GroupView& grp,
+                         GridSync* gs, int* iters, int* info, cudaStream_t st) {
+  using namespace node;
+  const int cmax = nc < nt ? nc : nt;
+  const size_t Pmax = (size_t)cmax * nb;
+  double* H = scratch;
+  double* Jb = H + Pmax * N;
+  double* R = Jb + Pmax * N * N;
+  double* recs = R + Pmax * N;
+  cudaError_t e;
+  int step = 0, chunk = 0;
+  info[0] = 0;
+  auto flags = [&](unsigned& f) -> cudaError_t {
+    if (grp.world > 1) node_group_flags_kernel<<<1, 32, 0, st>>>(grp, gs, d_flags, 60ull * 1000 * 1000 * 1000);
+    cudaError_t ee = cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    if (ee == cudaSuccess) ee = cudaStreamSynchronize(st);
+    f = *h_flags;
+    return ee;
+  };
+  while (step < nt) {
+    const int c = min(nc, nt - step);
+    const int P = c * nb;
+    node_init_chunk_kernel<<<blocks_for((size_t)P * N, 256), 256, 0, st>>>(states, dy, step, c, nb);
+    if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, 1, tol_a,
+                                                               tol_r, d_flags);
+    unsigned f = 0;
+    if ((e = flags(f)) != cudaSuccess) return e;
+    int it = 0;
+    if (f & FLAG_TIMEOUT) return info[0] = 4, cudaSuccess;
+    if (f & FLAG_NON_FINITE) return info[0] = 2, info[1] = step + 1, info[2] = 0, cudaSuccess;
+    while (f & FLAG_NOT_CONVERGED) {
+      if (it == max_iter) return info[0] = 2, info[1] = step + 1, info[2] = max_iter, cudaSuccess;
+      ++it;
+      if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
+      node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step, c, nb, 0, recs, sing_key, 0, nc);
+      node_thomas_fwd_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(states, R, recs, step, c, nb);
+      if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
+      if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+      node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, 0, tol_a,
+                                                                 tol_r, d_flags);
+      if ((e = flags(f)) != cudaSuccess) return e;
+      unsigned long long key = ~0ull;
+      if ((e = cudaMemcpyAsync(h_flags + 2, sing_key, sizeof key, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return e;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+      std::memcpy(&key, h_flags + 2, sizeof key);
+      if (f & FLAG_TIMEOUT) return info[0] = 4, cudaSuccess;
+      if (key != ~0ull) return info[0] = 1, info[1] = step + 1, info[2] = it, cudaSuccess;
+      if (f & FLAG_NON_FINITE) return info[0] = 2, info[1] = step + 1, info[2] = it, cudaSuccess;
+    }
+    iters[chunk] = it;
+    step += c;
+    ++chunk;
+  }
+  info[3] = chunk;
+  return cudaSuccess;
+}
+
+// Adjoint over a trajectory for the wide neural ODE (Thomas solver); writes the
+// quadrature weights wq and the final lambda.
+cudaError_t node_adjoint(const DevModel& m, const double* states, const double* times, const double* dL,
+                         const double* loss, int nb, int nt, int nc, double* scratch, double* lam, double* wq,
+                         unsigned long long* sing_key, cudaStream_t st) {
+  using namespace node;
+  const int cmax = nc < nt ? nc : nt;
+  const size_t Pmax = (size_t)cmax * nb;
+  double* H = scratch;
+  double* Jb = H + Pmax * N;
+  double* R = Jb + Pmax * N * N;
+  double* recs = R + Pmax * N;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(lam, 0, sizeof(double) * (size_t)nb * N, st)) != cudaSuccess) return e;
+  int step_hi = nt;
+  unsigned long long ord = 0;
+  while (step_hi >= 1) {
+    const int c = min(nc, step_hi);
+    const int P = c * nb;
+    // row r of the chunk is trajectory step step_hi - r
+    if ((e = node_eval(m, states, times, step_hi, -1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
+    node_adj_rhs_kernel<<<blocks_for(P, 128), 128, 0, st>>>(states, times, Jb, dL, loss, lam, step_hi, c, nb, R);
+    node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step_hi, c, nb, 1, recs, sing_key, ord, nc);
+    node_thomas_adj_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(R, recs, times, step_hi, c, nb, lam, wq);
+    step_hi -= c;
+    ++ord;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cko
