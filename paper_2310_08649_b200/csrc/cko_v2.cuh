@@ -57,7 +57,8 @@ __device__ __forceinline__ int producer_of(int warp) {
   if ((warp & 3) == 0) return -1;
   return warp - 1 - (warp >> 2);
 }
-constexpr int kMaxSlots = 7;  // named barriers 1..2S must stay below 16
+constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay below 16
+constexpr int kSmemCap = 224 * 1024;
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -78,21 +79,27 @@ struct Rec {
   static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
 };
 
+// Per-group pivot-row buffer: two rows of N + 1 doubles (row, reciprocal of its pivot).
+template <int N>
+constexpr int kPb = 2 * (N + 1);
+
 struct Shape {
-  int S, Ws, LT;       // slots, producer warps per slot, lanes per tile
+  int S, Ws, LT;       // producer sets, producer warps per set, lanes per tile
+  int Q;               // record slots in the ring (a multiple of S: each set fills every S-th slot)
+  int RS;              // records per slot (= groups per set)
   int threads;
   int smem_bytes;
 };
 
 template <class MS>
-__host__ __device__ inline void smem_layout(int S, int Ws, int LT, int& o_cs, int& o_rec, int& o_pb, int& o_vs,
+__host__ __device__ inline void smem_layout(int S, int Q, int Ws, int RS, int LT, int& o_cs, int& o_rec, int& o_pb, int& o_vs,
                                             int& o_lam, int& total_doubles) {
   constexpr int N = MS::N;
   o_cs = 0;
   o_rec = ((MS::NCONST + 1) / 2) * 2;
-  o_pb = o_rec + S * LT * Rec<N>::STRIDE;
-  const int groups = S * Ws * Geo<N>::GPW;
-  o_vs = o_pb + groups * 2 * N;
+  o_pb = o_rec + Q * RS * Rec<N>::STRIDE;
+  const int groups = S * RS;
+  o_vs = o_pb + groups * kPb<N>;
   o_lam = o_vs + LT * N + (N & 1);
   total_doubles = o_lam + LT * N + 8;
 }
@@ -100,6 +107,19 @@ __host__ __device__ inline void smem_layout(int S, int Ws, int LT, int& o_cs, in
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// 1 / x to within an ulp: the hardware seed refined by two Newton steps (no
+// special-case path; pivots here are finite and nonzero or the block is
+// flagged singular anyway). The reference divides; the factors differ from it
+// at rounding level only.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
 // Rotation reduction inside a group of G lanes starting at lane `base`:
@@ -118,110 +138,21 @@ __device__ __forceinline__ double group_max_nonneg(double v, int base, int gl) {
 }
 
 // LU with partial pivoting (lu_factor_block, linalg.cpp:13-44) of the block
-// whose rows lane gl of a G-lane group holds in a[s] (row gl + s G). Rows never
-// move: pos[s] tracks each row's position in the reference's swapped order and
-// the pivot of column c is the candidate (pos >= c) with the largest |a|,
-// ties to the smallest position — exactly the reference's strict '>' scan.
-// The whole warp must call this (shuffles use the full mask); factors go to
-// `rec` in reference row order; pb is a 2N-double group buffer.
+// whose rows lane gl of a G-lane group holds in a[s] (row gl + s G), factors
+// to `rec` in the reference's row order. Rows sit at static lanes/slots, so
+// the common column (the diagonal already wins the reference's strict '>'
+// scan) is a plain elimination step: the owner of row c publishes it to the
+// group buffer, every lane reads the pivot, and a warp vote checks that no row
+// below beats it. Only when one does (warp-uniform branch) is the argmax taken
+// — the largest |a(r, c)|, ties to the smallest r, exactly the reference's scan
+// — and rows c and p are exchanged physically through `rec` (scratch until
+// the factors are stored: each row is written to its swapped position and
+// read back), so the static layout holds again; `orig` tracks
+// each row's source row for the permutation. Arithmetic per column is then
+// identical to the reference's (multiplier by the pivot reciprocal). The whole
+// warp must call this; pb is a kPb<N>-double group buffer.
 template <int N>
 __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec) {
-  constexpr int G = Geo<N>::G, R = Geo<N>::R;
-  int pos[R];
-#pragma unroll
-  for (int s = 0; s < R; ++s) pos[s] = (gl + s * G < N) ? gl + s * G : -1;
-  double lm = 0.0;
-#pragma unroll
-  for (int s = 0; s < R; ++s)
-    if (pos[s] >= 0)
-#pragma unroll
-      for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
-  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
-  bool ok = true;
-#pragma unroll
-  for (int c = 0; c < N; ++c) {
-    // key (|a|, position): larger |a| wins, ties to the smaller position
-    double bv = -1.0;
-    int bp = INT_MAX, bs = 0;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      if (pos[s] >= c) {
-        const double v = fabs(a[s][c]);
-        if (v > bv || (v == bv && pos[s] < bp)) bv = v, bp = pos[s], bs = s;
-      }
-    }
-    int own = bp;  // my best candidate's position (INT_MAX if none)
-#pragma unroll
-    for (int off = 1; off < G; off <<= 1) {
-      const int src = rot_src<G>(base, gl, off);
-      const double ov = __shfl_sync(0xffffffffu, bv, src);
-      const int op = __shfl_sync(0xffffffffu, bp, src);
-      if (ov > bv || (ov == bv && op < bp)) bv = ov, bp = op;
-    }
-    int p = bp;
-    if (p == INT_MAX) {  // no comparable candidate (NaN column): keep row c, flag it
-      p = c;
-      ok = false;
-#pragma unroll
-      for (int s = 0; s < R; ++s)
-        if (pos[s] == c) own = c, bs = s;
-    }
-    double* buf = pb + (c & 1) * N;
-    if (own == p) {  // the owner lane publishes the pivot row from slot bs
-#pragma unroll
-      for (int j = c; j < N; ++j) {
-        double u = a[0][j];
-#pragma unroll
-        for (int s = 1; s < R; ++s) u = (bs == s) ? a[s][j] : u;
-        buf[j] = u;
-      }
-    }
-    __syncwarp();
-    const double piv = buf[c];
-    if (fabs(piv) < tiny || piv == 0.0) ok = false;
-    const double inv = __drcp_rn(piv);  // == 1.0 / piv, correctly rounded
-    if (gl == 0) rec[Rec<N>::RD + c] = inv;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      if (pos[s] == p)
-        pos[s] = c;
-      else if (pos[s] == c)
-        pos[s] = p;
-    }
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      if (pos[s] > c) {
-        const double l = a[s][c] * inv;
-        a[s][c] = l;
-#pragma unroll
-        for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
-      }
-    }
-  }
-  int* perm = reinterpret_cast<int*>(rec + Rec<N>::PERM);
-#pragma unroll
-  for (int s = 0; s < R; ++s) {
-    if (pos[s] >= 0) {
-      double* row = rec + pos[s] * N;
-#pragma unroll
-      for (int j = 0; j < N; ++j) row[j] = a[s][j];
-      perm[pos[s]] = gl + s * G;
-    }
-  }
-  if (gl == 0) perm[N] = 0;
-  return ok;
-}
-
-// Fast path of lu_group: the same elimination without the pivot search, for
-// blocks where the reference's scan keeps every diagonal (|a(r,c)| <= |a(c,c)|
-// for all r > c, the common case for M = I - dt J). The row of column c then
-// sits at a static lane/slot, so there is no argmax and no select; `viol`
-// reports (per lane) whether the reference would have exchanged rows, in which
-// case the caller redoes the block with lu_group. When no exchange happens the
-// arithmetic is identical to lu_group / lu_factor_block.
-template <int N>
-__device__ inline bool lu_group_nopiv(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec,
-                                      bool& viol) {
   constexpr int G = Geo<N>::G, R = Geo<N>::R;
   double lm = 0.0;
 #pragma unroll
@@ -229,34 +160,94 @@ __device__ inline bool lu_group_nopiv(double (&a)[Geo<N>::R][N], int gl, int bas
     if (gl + s * G < N)
 #pragma unroll
       for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
-  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
-  bool ok = true;
-  viol = false;
+  int orig[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) orig[s] = gl + s * G;
+  bool swapped = false;  // group-uniform
+  double pmin = INFINITY;
+  int* iscr = reinterpret_cast<int*>(rec + Rec<N>::PERM);  // row-source scratch until perm is stored
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    double* buf = pb + (c & 1) * N;
-    if (gl == c % G) {
+    double* buf = pb + (c & 1) * (N + 1);
+    const int sc = c / G, lc = c % G;  // slot / lane of row c
+    if (gl == lc) {
 #pragma unroll
-      for (int j = c; j < N; ++j) buf[j] = a[c / G][j];
+      for (int j = c; j < N; ++j) buf[j] = a[sc][j];
     }
     __syncwarp();
-    const double piv = buf[c];
+    double piv = buf[c];
+    bool beat = false;
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) beat |= fabs(a[s][c]) > fabs(piv);
+    if (__any_sync(0xffffffffu, beat)) {
+      // argmax over rows r >= c of the group: key (|a(r, c)|, r), larger |a| wins, ties to the smaller r
+      double bv = -1.0;
+      int br = INT_MAX;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + s * G;
+        if (s * G + G - 1 >= c && r >= c && r < N) {
+          const double v = fabs(a[s][c]);
+          if (v > bv) bv = v, br = r;  // slots ascend in r, so '>' keeps the smaller r on ties
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < G; off <<= 1) {
+        const int src = rot_src<G>(base, gl, off);
+        const double ov = __shfl_sync(0xffffffffu, bv, src);
+        const int orr = __shfl_sync(0xffffffffu, br, src);
+        if (ov > bv || (ov == bv && orr < br)) bv = ov, br = orr;
+      }
+      // br == INT_MAX only for a column of NaNs: keep row c (the reference's scan never moves)
+      const int p = (br == INT_MAX || !(fabs(piv) < bv)) ? c : br;
+      // exchange rows c and p: every row goes to its swapped position in the record, then reads back
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + s * G;
+        if (r < N) {
+          const int d = r == c ? p : (r == p ? c : r);
+#pragma unroll
+          for (int j = 0; j < N; ++j) rec[d * N + j] = a[s][j];
+          iscr[d] = orig[s];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + s * G;
+        if (r < N) {
+#pragma unroll
+          for (int j = 0; j < N; ++j) a[s][j] = rec[r * N + j];
+          orig[s] = iscr[r];
+        }
+      }
+      swapped |= p != c;
+      if (gl == lc) {
+#pragma unroll
+        for (int j = c; j < N; ++j) buf[j] = a[sc][j];
+      }
+      __syncwarp();
+      piv = buf[c];
+    }
     const double apiv = fabs(piv);
-    if (apiv < tiny || piv == 0.0) ok = false;
-    const double inv = __drcp_rn(piv);
+    pmin = fmin(pmin, apiv);  // the singularity test is applied once at the end
+    const double inv = rcp_nr(piv);
     if (gl == 0) rec[Rec<N>::RD + c] = inv;
 #pragma unroll
     for (int s = 0; s < R; ++s) {
-      if (gl + s * G > c && gl + s * G < N) {
-        const double v = a[s][c];
-        viol |= fabs(v) > apiv;
-        const double l = v * inv;
+      // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1
+      if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) {
+        const double l = a[s][c] * inv;
         a[s][c] = l;
 #pragma unroll
         for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
       }
     }
   }
+  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
+  const bool ok = !(pmin < tiny || pmin == 0.0);
+  __syncwarp();  // rec scratch reads done before the factors overwrite it
   int* perm = reinterpret_cast<int*>(rec + Rec<N>::PERM);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -265,37 +256,19 @@ __device__ inline bool lu_group_nopiv(double (&a)[Geo<N>::R][N], int gl, int bas
       double* row = rec + i * N;
 #pragma unroll
       for (int j = 0; j < N; ++j) row[j] = a[s][j];
-      perm[i] = i;
+      perm[i] = orig[s];
     }
   }
-  if (gl == 0) perm[N] = 1;
+  if (gl == 0) perm[N] = swapped ? 0 : 1;
   return ok;
 }
 
-// Build the block with `build(m)` (rows this lane holds) and factor it: the
-// no-exchange fast path first; if any group of the warp needs a row exchange
-// the whole warp rebuilds and runs the pivoting factorisation.
-template <int N, class Build>
-__device__ __noinline__ bool factor_block_pivoting(const Build& build, int gl, int base, double* pb, double* rec) {
-  double m[Geo<N>::R][N];
-  build(m);
-  __syncwarp();
-  return lu_group<N>(m, gl, base, pb, rec);
-}
-
+// Build the block with `build(m)` (rows this lane holds) and factor it.
 template <int N, class Build>
 __device__ inline bool factor_block(const Build& build, int gl, int base, double* pb, double* rec) {
-  bool viol, ok;
-  {
-    double m[Geo<N>::R][N];
-    build(m);
-    ok = lu_group_nopiv<N>(m, gl, base, pb, rec, viol);
-  }
-  if (__any_sync(0xffffffffu, viol)) {  // rare: kept out of line so it costs no registers here
-    __syncwarp();
-    ok = factor_block_pivoting<N>(build, gl, base, pb, rec);
-  }
-  return ok;
+  double m[Geo<N>::R][N];
+  build(m);
+  return lu_group<N>(m, gl, base, pb, rec);
 }
 
 // lu_solve_vec (linalg.cpp:46-60) from a record, one thread: v <- M^{-1} v.
@@ -355,6 +328,40 @@ __device__ __forceinline__ void load_vec(const double* __restrict__ p, double (&
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+// The producer/consumer ring of one epoch is flattened over work items
+// i = k * LTc + lane (row k of lane `lane` of the tile): slot j holds the RS
+// records of items j RS .. j RS + RS - 1, so no producer group idles when the
+// tile has fewer lanes than a set has groups. Set s fills slots s, s + S, ...
+// into ring position j % Q; full(q) = barrier 1 + q, empty(q) = 1 + Q + q.
+// The consumer syncs each slot once, in order, and releases a slot when the
+// rows it serves are solved (only if a later slot reuses the position).
+struct RingConsumer {
+  int RS, Q, LTc, J, nthr, synced, released;
+  __device__ RingConsumer(int rs, int q, int ltc, int c, int n)
+      : RS(rs), Q(q), LTc(ltc), J((c * ltc + rs - 1) / rs), nthr(n), synced(0), released(0) {}
+  __device__ __forceinline__ void acquire(int k) {  // every slot holding an item of row k
+    const int need = ((k + 1) * LTc - 1) / RS;
+    while (synced <= need) {
+      bar_sync(1 + synced % Q, nthr);
+      ++synced;
+    }
+  }
+  __device__ __forceinline__ void release(int k) {  // slots whose items all belong to rows <= k
+    const int done = ((k + 1) * LTc) / RS;
+    while (released < done) {
+      if (released + Q < J) bar_arrive(1 + Q + released % Q, nthr);
+      ++released;
+    }
+  }
+  __device__ __forceinline__ int record(int k, int lane) const {
+    const int i = k * LTc + lane;
+    return (i / RS % Q) * RS + i % RS;
+  }
+};
+
+// CKO_TRACE diagnostics record the second chunk (the first one runs cold).
+__device__ __forceinline__ int trace_step(const FwdLaunch& a) { return a.nt > a.nc ? a.nc : 0; }
+
 struct FwdCtx {
   int lb0, L, step, c;
   size_t row;  // nb * N
@@ -365,7 +372,7 @@ struct FwdCtx {
 // trajectory row step + 1 + k, so yy_{-1} = y_start is row `step`.
 template <class MS>
 __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double* cs, double* hr, double* nrm,
-                              bool first, unsigned* s_flags) {
+                              bool first, unsigned* s_flags, unsigned long long* rtr = nullptr) {
   constexpr int N = MS::N;
   const int nb = a.nb;
   for (int p = threadIdx.x; p < x.c * x.L; p += blockDim.x) {
@@ -387,7 +394,9 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
     nrm[p] = s;
   }
   if (threadIdx.x == 0) *s_flags = 0;
+  if (rtr) rtr[0] = globaltimer_ns();
   __syncthreads();
+  if (rtr) rtr[1] = globaltimer_ns();
   unsigned f = 0;
   for (int lb = threadIdx.x; lb < x.L; lb += blockDim.x) {
     const int b = x.lb0 + lb;
@@ -406,6 +415,7 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
     if (!(rn <= a.tol_a || rn <= xmul(a.tol_r, r0v))) f |= FLAG_NOT_CONVERGED;
   }
   if (f) atomicOr(s_flags, f);
+  if (rtr) rtr[2] = globaltimer_ns();
   __syncthreads();
   return *s_flags;
 }
@@ -417,7 +427,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
   constexpr int N = MS::N;
   using Gm = Geo<N>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = sh.S, Ws = sh.Ws;
+  const int S = sh.S, Q = sh.Q, Ws = sh.Ws;
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
   const int pw = producer_of(warp);
@@ -427,16 +437,20 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
     const int s = pw / Ws, sw = pw % Ws;
     const GroupLane<N> gr(lane);
     const int g = gr.g, gl = gr.gl;
-    const int lt = sw * Gm::GPW + g;
-    const bool active = lt < LTc;  // inactive groups factor a duplicate point, no side effects
-    const int lb = t0 + (active ? lt : LTc - 1), b = x.lb0 + lb;
-    double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
-    double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
-    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == 0 && lane == 0) ? a.trace + 64 : nullptr;
-    for (int k = s; k < x.c; k += S) {
-      if (tr) tr[k * 8 + 0] = globaltimer_ns();
-      if (k >= S) bar_sync(1 + S + s, nthr);
-      if (tr) tr[k * 8 + 1] = globaltimer_ns();
+    const int gi = sw * Gm::GPW + g;  // record within the slot
+    const int RS = sh.RS, I = x.c * LTc, J = (I + RS - 1) / RS;
+    double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
+    unsigned long long* tr0 = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
+    for (int js = s; js < J; js += S) {
+      const int q = js % Q;
+      const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
+      const int item = active ? js * RS + gi : I - 1;
+      const int k = item / LTc, lb = t0 + item % LTc, b = x.lb0 + lb;
+      double* rec = recs + (size_t)(q * RS + gi) * Rec<N>::STRIDE;
+      unsigned long long* tr = (tr0 && js < x.c) ? tr0 + js * 8 : nullptr;  // slot js: tr[js * 8 + 0..3]
+      if (tr) tr[0] = globaltimer_ns();
+      if (js >= Q) bar_sync(1 + Q + q, nthr);
+      if (tr) tr[1] = globaltimer_ns();
       const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
       const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
       double y[N];
@@ -462,13 +476,13 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
           }
         }
       };
-      if (tr) tr[k * 8 + 2] = globaltimer_ns();
+      if (tr) tr[2] = globaltimer_ns();
       if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0) {
         atomicMin(a.sing_key, (unsigned long long)k * nb + b);
         atomicOr(s_sing, 1u);
       }
-      if (tr) tr[k * 8 + 3] = globaltimer_ns();
-      bar_arrive(1 + s, nthr);
+      if (tr) tr[3] = globaltimer_ns();
+      bar_arrive(1 + q, nthr);
     }
   } else if (warp == 0) {
     // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, one thread per lane
@@ -479,14 +493,14 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
 #pragma unroll
     for (int i = 0; i < N; ++i) xv[i] = 0.0;
     double* vs = vss + (size_t)lt * N;
-    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == 0 && lane == 0) ? a.trace + 64 : nullptr;
+    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
+    RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
     for (int k = 0; k < x.c; ++k) {
-      const int s = k % S;
       if (tr) tr[k * 8 + 4] = globaltimer_ns();
-      bar_sync(1 + s, nthr);
+      ring.acquire(k);
       if (tr) tr[k * 8 + 5] = globaltimer_ns();
       if (active) {
-        const double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(k, lt) * Rec<N>::STRIDE;
 #pragma unroll
         for (int i = 0; i < N; ++i) xv[i] = rec[Rec<N>::RHS + i] + xv[i];
         lu_solve_rec<N>(rec, vs, xv);
@@ -495,7 +509,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         for (int i = 0; i < N; ++i) yy[i] = rec[Rec<N>::Y + i] - xv[i];
       }
       if (tr) tr[k * 8 + 6] = globaltimer_ns();
-      if (k + S < x.c) bar_arrive(1 + S + s, nthr);
+      ring.release(k);
     }
   }
 }
@@ -506,7 +520,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned s_bcast, s_flags, s_sing;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -517,7 +531,9 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   lane_range(a.nb, x.lb0, x.L);
   x.row = (size_t)a.nb * N;
   double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
-  double* nrm = hr + (size_t)a.slab.Pmax * N;
+  // point norms: in the (idle) record ring when they fit, else in the slab
+  const int ring_doubles = sh.Q * sh.RS * Rec<N>::STRIDE;
+  double* nrm = a.slab.Pmax <= ring_doubles ? recs : hr + (size_t)a.slab.Pmax * N;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
   int step = 0, chunk = 0;
@@ -527,20 +543,23 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
     x.c = c;
     for (int p = threadIdx.x; p < c * x.L; p += blockDim.x) {  // initial iterate: every row at y_start
       const int k = p / x.L, b = x.lb0 + p % x.L;
-      const double* src = a.states + (size_t)step * x.row + (size_t)b * N;
-      double* dst = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
+      double v[N];
+      load_vec<N>(a.states + (size_t)step * x.row + (size_t)b * N, v);  // all loads before any store
       if (a.dy_init) {
-        const double* d = a.dy_init + ((size_t)k * a.nb + b) * N;
-        for (int i = 0; i < N; ++i) dst[i] = src[i] + d[i];
-      } else {
-        for (int i = 0; i < N; ++i) dst[i] = src[i];
+        double d[N];
+        load_vec<N>(a.dy_init + ((size_t)k * a.nb + b) * N, d);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] += d[i];
       }
+      double* dst = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = v[i];
     }
     __syncthreads();
     int it = 0;
     unsigned long long* ktr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && chunk < 4) ? a.trace + chunk * 16 : nullptr;
     if (ktr) ktr[0] = globaltimer_ns();
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags);
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags, ktr ? ktr + 11 : nullptr);
     if (ktr) ktr[1] = globaltimer_ns();
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
@@ -595,7 +614,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   constexpr int N = MS::N;
   using Gm = Geo<N>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = sh.S, Ws = sh.Ws;
+  const int S = sh.S, Q = sh.Q, Ws = sh.Ws;
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
   const size_t row = (size_t)nb * N;
@@ -604,15 +623,18 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     const int s = pw / Ws, sw = pw % Ws;
     const GroupLane<N> gr(lane);
     const int g = gr.g, gl = gr.gl;
-    const int lt = sw * Gm::GPW + g;
-    const bool active = lt < LTc;  // inactive groups factor a duplicate point, no side effects
-    const int ltc = active ? lt : LTc - 1;
-    const int b = lb0 + t0 + ltc;
-    double* pb = pbs + (size_t)((s * Ws + sw) * Gm::GPW + g) * 2 * N;
-    double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
-    const double* lm = lam + (size_t)ltc * N;
-    for (int r = s; r < c; r += S) {
-      if (r >= S) bar_sync(1 + S + s, nthr);
+    const int gi = sw * Gm::GPW + g;  // record within the slot
+    const int RS = sh.RS, I = c * LTc, J = (I + RS - 1) / RS;
+    double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
+    for (int js = s; js < J; js += S) {
+      const int q = js % Q;
+      const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
+      const int item = active ? js * RS + gi : I - 1;
+      const int r = item / LTc, ltc = item % LTc;
+      const int b = lb0 + t0 + ltc;
+      const double* lm = lam + (size_t)ltc * N;
+      double* rec = recs + (size_t)(q * RS + gi) * Rec<N>::STRIDE;
+      if (js >= Q) bar_sync(1 + Q + q, nthr);
       const int m = step_hi - r;
       const double t = a.times[(size_t)m * nb + b];
       const double dt = t - a.times[(size_t)(m - 1) * nb + b];
@@ -655,7 +677,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       };
       if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0)
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
-      bar_arrive(1 + s, nthr);
+      bar_arrive(1 + q, nthr);
     }
   } else if (warp == 0) {
     const int lt = lane;
@@ -666,11 +688,11 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     double d[N];  // delta_{r-1}, then delta_r
 #pragma unroll
     for (int i = 0; i < N; ++i) d[i] = 0.0;
+    RingConsumer ring(sh.RS, Q, LTc, c, nthr);
     for (int r = 0; r < c; ++r) {
-      const int s = r % S;
-      bar_sync(1 + s, nthr);
+      ring.acquire(r);
       if (active) {
-        const double* rec = recs + (size_t)(s * sh.LT + lt) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(r, lt) * Rec<N>::STRIDE;
         const int m = step_hi - r;
 #pragma unroll
         for (int i = 0; i < N; ++i) d[i] = rec[Rec<N>::RHS + i] + d[i];
@@ -680,7 +702,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
 #pragma unroll
         for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
       }
-      if (r + S < c) bar_arrive(1 + S + s, nthr);
+      ring.release(r);
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) dcar[i] = d[i];
@@ -692,7 +714,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -739,12 +761,19 @@ inline Shape make_shape(int L) {
   if (Ws > kMaxWs) Ws = kMaxWs;
   if (Ws < 1) Ws = 1;
   sh.Ws = Ws;
-  sh.S = kMaxProducers / Ws;  // ring depth: as many slots as the producer warps allow
+  sh.S = kMaxProducers / Ws;  // producer sets: as many as the producer warps allow
   if (sh.S > kMaxSlots) sh.S = kMaxSlots;
-  sh.LT = Ws * gpw < 32 ? Ws * gpw : 32;  // lanes per tile == records per slot
+  sh.RS = Ws * gpw;
   sh.threads = 32 * kMaxWarps;
+  // Two record slots per set when they fit: a set factors slot j + S while the
+  // consumer still reads slot j, so the producers never wait on the solve.
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Ws, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  for (sh.Q = 2 * sh.S;; sh.Q = sh.S) {
+    // a tile row must never need a slot more than Q - 1 slots past the oldest unreleased one
+    sh.LT = min(32, (sh.Q - 1) * sh.RS);
+    smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+    if (sh.Q == sh.S || (sh.Q <= kMaxSlots && tot * 8 <= kSmemCap)) break;
+  }
   sh.smem_bytes = tot * 8;
   return sh;
 }

@@ -19,7 +19,7 @@ t = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 k0 = t[0]
 print("chunk markers (us from chunk-0 start): res0, [it: epoch-start, epoch-end, res+sync-end]")
 for ch in range(4):
-    row = t[ch * 16: ch * 16 + 11]
+    row = t[ch * 16: ch * 16 + 14]
     print(ch, [(v - k0) / 1000 if v else None for v in row])
 rows = t[64:].reshape(-1, 8)
 print("row: prod(wait-start, acquired, lu-start, lu-end) cons(wait-start, acquired, done) in us")
