@@ -512,7 +512,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   static const char* trace_path = std::getenv("CKO_TRACE");
   Buf tbuf;
   if (trace_path && v2) {
-    CUDA_TRY(tbuf.ensure(sizeof(unsigned long long) * (64 + 8 * (size_t)nc_eff)));
+    CUDA_TRY(tbuf.ensure(sizeof(unsigned long long) * (64 + 8 * (size_t)nc_eff + 8 * (size_t)G)));
     CUDA_TRY(cudaMemsetAsync(tbuf.p, 0, tbuf.bytes, c->stream));
     a.trace = tbuf.as<unsigned long long>();
   }

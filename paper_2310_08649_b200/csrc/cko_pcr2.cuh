@@ -283,18 +283,23 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
     PcrCtx pc{pcr_workspace<MS>(a.slab, smem + OCS, in_smem != 0, c, x.L), x.L, c, a.solver == 1 ? -1 : a.n_switch};
     for (int p = tid; p < c * x.L; p += T) {  // initial iterate: every row at y_start
       const int k = p / x.L, b = x.lb0 + p % x.L;
-      const double* src = a.states + (size_t)step * x.row + (size_t)b * N;
-      double* dst = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
+      double v[N];
+      load_vec<N>(a.states + (size_t)step * x.row + (size_t)b * N, v);  // all loads before any store
       if (a.dy_init) {
-        const double* d = a.dy_init + ((size_t)k * nb + b) * N;
-        for (int i = 0; i < N; ++i) dst[i] = src[i] + d[i];
-      } else {
-        for (int i = 0; i < N; ++i) dst[i] = src[i];
+        double d[N];
+        load_vec<N>(a.dy_init + ((size_t)k * nb + b) * N, d);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] += d[i];
       }
+      double* dst = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) dst[i] = v[i];
     }
     __syncthreads();
     int it = 0;
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags);
+    // residual staging in the (idle) shared-memory PCR workspace, if it lives there
+    const int stage_cap = in_smem ? (int)(dyn_smem_bytes() / 8) - OCS : 0;
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, true, &s_flags);
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
       if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
       }
       __syncthreads();
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
-      f = residual2<MS>(a, x, cs, hr, nrm, false, &s_flags) | fl;
+      f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, false, &s_flags) | fl;
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
       if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
         if (leader) {

@@ -59,6 +59,8 @@ __device__ __forceinline__ int producer_of(int warp) {
 }
 constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay below 16
 constexpr int kSmemCap = 224 * 1024;
+constexpr int kRoundBarrier = 15;
+constexpr bool kFwdRounds = false;  // producers only; ring barriers use 1 .. 2Q <= 14
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -137,6 +139,32 @@ __device__ __forceinline__ double group_max_nonneg(double v, int base, int gl) {
   return v;
 }
 
+// Row moves through shared memory, 16-byte accesses when rows stay aligned.
+template <int N>
+__device__ __forceinline__ void store_row(double* dst, const double (&v)[N]) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(v[j], v[j + 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) dst[j] = v[j];
+  }
+}
+template <int N>
+__device__ __forceinline__ void load_row(const double* src, double (&v)[N]) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(src + j);
+      v[j] = t.x;
+      v[j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) v[j] = src[j];
+  }
+}
+
 // LU with partial pivoting (lu_factor_block, linalg.cpp:13-44) of the block
 // whose rows lane gl of a G-lane group holds in a[s] (row gl + s G), factors
 // to `rec` in the reference's row order. Rows sit at static lanes/slots, so
@@ -181,34 +209,28 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
     for (int s = 0; s < R; ++s)
       if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) beat |= fabs(a[s][c]) > fabs(piv);
     if (__any_sync(0xffffffffu, beat)) {
-      // argmax over rows r >= c of the group: key (|a(r, c)|, r), larger |a| wins, ties to the smaller r
-      double bv = -1.0;
-      int br = INT_MAX;
+      // the reference's scan (strict '>' from row c down) over |a(r, c)| staged in the idle half of pb
+      double* cand = pb + ((c + 1) & 1) * (N + 1);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int r = gl + s * G;
-        if (s * G + G - 1 >= c && r >= c && r < N) {
-          const double v = fabs(a[s][c]);
-          if (v > bv) bv = v, br = r;  // slots ascend in r, so '>' keeps the smaller r on ties
-        }
+        if (s * G + G - 1 >= c && r >= c && r < N) cand[r] = fabs(a[s][c]);
       }
-#pragma unroll
-      for (int off = 1; off < G; off <<= 1) {
-        const int src = rot_src<G>(base, gl, off);
-        const double ov = __shfl_sync(0xffffffffu, bv, src);
-        const int orr = __shfl_sync(0xffffffffu, br, src);
-        if (ov > bv || (ov == bv && orr < br)) bv = ov, br = orr;
+      __syncwarp();
+      int p = c;
+      double bv = cand[c];
+#pragma unroll 1
+      for (int r = c + 1; r < N; ++r) {
+        const double v = cand[r];
+        if (v > bv) bv = v, p = r;
       }
-      // br == INT_MAX only for a column of NaNs: keep row c (the reference's scan never moves)
-      const int p = (br == INT_MAX || !(fabs(piv) < bv)) ? c : br;
       // exchange rows c and p: every row goes to its swapped position in the record, then reads back
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int r = gl + s * G;
         if (r < N) {
           const int d = r == c ? p : (r == p ? c : r);
-#pragma unroll
-          for (int j = 0; j < N; ++j) rec[d * N + j] = a[s][j];
+          store_row<N>(rec + d * N, a[s]);
           iscr[d] = orig[s];
         }
       }
@@ -217,8 +239,7 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
       for (int s = 0; s < R; ++s) {
         const int r = gl + s * G;
         if (r < N) {
-#pragma unroll
-          for (int j = 0; j < N; ++j) a[s][j] = rec[r * N + j];
+          load_row<N>(rec + r * N, a[s]);
           orig[s] = iscr[r];
         }
       }
@@ -253,9 +274,7 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
   for (int s = 0; s < R; ++s) {
     const int i = gl + s * G;
     if (i < N) {
-      double* row = rec + i * N;
-#pragma unroll
-      for (int j = 0; j < N; ++j) row[j] = a[s][j];
+      store_row<N>(rec + i * N, a[s]);
       perm[i] = orig[s];
     }
   }
@@ -367,31 +386,111 @@ struct FwdCtx {
   size_t row;  // nb * N
 };
 
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+
 // Residual + lane norms for all c x L points of this CTA (rate_residual_norms,
 // integrate.cpp:64-95). The chunk's iterate yy_k lives in its final place,
 // trajectory row step + 1 + k, so yy_{-1} = y_start is row `step`.
 template <class MS>
 __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double* cs, double* hr, double* nrm,
-                              bool first, unsigned* s_flags, unsigned long long* rtr = nullptr) {
+                              double* stage, int cap, bool first, unsigned* s_flags,
+                              unsigned long long* rtr = nullptr) {
   constexpr int N = MS::N;
-  const int nb = a.nb;
-  for (int p = threadIdx.x; p < x.c * x.L; p += blockDim.x) {
-    const int k = p / x.L, lb = p % x.L, b = x.lb0 + lb;
-    const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
-    const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
-    double y[N], ym[N], h[N];
-    load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
-    load_vec<N>(a.states + (size_t)(x.step + k) * x.row + (size_t)b * N, ym);
-    MS::rate(a.m, cs, t, y, h, b);
-    double s = 0.0;
-    double* o = hr + (size_t)p * N;
+  const int nb = a.nb, L = x.L, LN = L * N, P = x.c * L;
+  // Staged in shared memory (the idle record ring): the CTA's lanes of one
+  // trajectory row are L N contiguous doubles, so rows come in and residuals
+  // go out (hr is point-major, contiguous over the chunk) fully coalesced.
+  if (P <= cap / 4) {  // point norms in shared memory too when they fit
+    nrm = stage + cap - P;
+    cap -= P;
+  }
+  const int KB = cap > LN + L ? (cap - LN - L) / (2 * LN + L) : 0;  // rows per staged block
+  if (KB < 1) {  // no room to stage: one point per thread straight from L2
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+      const int k = p / L, lb = p % L, b = x.lb0 + lb;
+      const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+      const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      double y[N], ym[N], h[N];
+      load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
+      load_vec<N>(a.states + (size_t)(x.step + k) * x.row + (size_t)b * N, ym);
+      MS::rate(a.m, cs, t, y, h, b);
+      double s = 0.0;
+      double* o = hr + (size_t)p * N;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
-      o[i] = v;
-      s = xadd(s, xmul(v, v));
+      for (int i = 0; i < N; ++i) {
+        const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
+        o[i] = v;
+        s = xadd(s, xmul(v, v));
+      }
+      nrm[p] = s;
     }
-    nrm[p] = s;
+  }
+  for (int k0 = 0; KB >= 1 && k0 < x.c; k0 += KB) {
+    const int kb = min(KB, x.c - k0);
+    double* Y = stage;              // trajectory rows step + k0 .. step + k0 + kb
+    double* T = Y + (kb + 1) * LN;  // their times
+    double* O = T + (kb + 1) * L;   // residuals of rows k0 .. k0 + kb - 1
+    const double* src = a.states + (size_t)(x.step + k0) * x.row + (size_t)x.lb0 * N;
+    // asynchronous copies: every element in flight at once instead of one L2 round trip per element
+    {
+      // thread -> (row, 16-byte unit): several rows per pass, no divisions in the loop
+      constexpr int U = N % 2 == 0 ? 2 : 1;  // doubles per copy unit (rows stay 16-byte aligned for even N)
+      const int W = LN / U, rpp = blockDim.x >= W ? blockDim.x / W : 1;
+      const int r0 = threadIdx.x / W, e0 = threadIdx.x - r0 * W;
+      if (r0 < rpp)
+        for (int rr = r0; rr <= kb; rr += rpp)
+          for (int e = e0; e < W; e += blockDim.x) {
+            if constexpr (U == 2)
+              cp_async16(Y + rr * LN + 2 * e, src + (size_t)rr * x.row + 2 * e);
+            else
+              cp_async8(Y + rr * LN + e, src + (size_t)rr * x.row + e);
+          }
+    }
+    const double* ts = a.times + (size_t)(x.step + k0) * nb + x.lb0;
+    for (int e = threadIdx.x; e < (kb + 1) * L; e += blockDim.x) {
+      const int rr = e / L;
+      cp_async8(T + e, ts + (size_t)rr * nb + (e - rr * L));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (rtr && k0 == 0) rtr[3] = globaltimer_ns();
+    for (int p = threadIdx.x; p < kb * L; p += blockDim.x) {
+      const int kk = p / L, lb = p - kk * L, b = x.lb0 + lb;
+      const double t = T[(kk + 1) * L + lb];
+      const double dt = t - T[kk * L + lb];
+      double y[N], ym[N], h[N];
+      load_vec<N>(Y + (kk + 1) * LN + lb * N, y);
+      load_vec<N>(Y + kk * LN + lb * N, ym);
+      MS::rate(a.m, cs, t, y, h, b);
+      double s = 0.0;
+      double* o = O + p * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
+        o[i] = v;
+        s = xadd(s, xmul(v, v));
+      }
+      nrm[k0 * L + p] = s;
+    }
+    __syncthreads();
+    if (rtr && k0 == 0) rtr[4] = globaltimer_ns();
+    double* dst = hr + (size_t)k0 * LN;
+    for (int e = threadIdx.x; e < kb * LN; e += blockDim.x) dst[e] = O[e];
+    __syncthreads();
   }
   if (threadIdx.x == 0) *s_flags = 0;
   if (rtr) rtr[0] = globaltimer_ns();
@@ -441,7 +540,11 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
     const int RS = sh.RS, I = x.c * LTc, J = (I + RS - 1) / RS;
     double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
     unsigned long long* tr0 = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
-    for (int js = s; js < J; js += S) {
+    for (int js0 = 0; js0 < J; js0 += S) {
+      // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
+      if (kFwdRounds && js0 > 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      const int js = js0 + s;
+      if (js >= J) continue;
       const int q = js % Q;
       const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
       const int item = active ? js * RS + gi : I - 1;
@@ -531,9 +634,9 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   lane_range(a.nb, x.lb0, x.L);
   x.row = (size_t)a.nb * N;
   double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
-  // point norms: in the (idle) record ring when they fit, else in the slab
+  // residual staging: the record ring (idle between epochs)
   const int ring_doubles = sh.Q * sh.RS * Rec<N>::STRIDE;
-  double* nrm = a.slab.Pmax <= ring_doubles ? recs : hr + (size_t)a.slab.Pmax * N;
+  double* nrm = hr + (size_t)a.slab.Pmax * N;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
   int step = 0, chunk = 0;
@@ -558,10 +661,16 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
     __syncthreads();
     int it = 0;
     unsigned long long* ktr = (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && chunk < 4) ? a.trace + chunk * 16 : nullptr;
+    // per-CTA timeline of the traced chunk: start, res0, barrier, epoch end, res, barrier
+    unsigned long long* ctr = (a.trace && threadIdx.x == 0 && step == trace_step(a))
+                                  ? a.trace + 64 + 8 * (size_t)min(a.nc, a.nt) + 8 * blockIdx.x : nullptr;
+    if (ctr) ctr[0] = globaltimer_ns();
     if (ktr) ktr[0] = globaltimer_ns();
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, true, &s_flags, ktr ? ktr + 11 : nullptr);
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, true, &s_flags, ktr ? ktr + 11 : nullptr);
     if (ktr) ktr[1] = globaltimer_ns();
+    if (ctr) ctr[1] = globaltimer_ns();
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
+    if (ctr) ctr[2] = globaltimer_ns();
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
       if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
       return;
@@ -579,8 +688,11 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
       }
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
       if (ktr && it < 4) ktr[3 + 3 * (it - 1)] = globaltimer_ns();
-      f = residual2<MS>(a, x, cs, hr, nrm, false, &s_flags) | fl;
+      if (ctr && it == 1) ctr[3] = globaltimer_ns();
+      f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, false, &s_flags) | fl;
+      if (ctr && it == 1) ctr[4] = globaltimer_ns();
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
+      if (ctr && it == 1) ctr[5] = globaltimer_ns();
       if (ktr && it < 4) ktr[4 + 3 * (it - 1)] = globaltimer_ns();
       if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
         if (leader) {
@@ -626,7 +738,11 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     const int gi = sw * Gm::GPW + g;  // record within the slot
     const int RS = sh.RS, I = c * LTc, J = (I + RS - 1) / RS;
     double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
-    for (int js = s; js < J; js += S) {
+    for (int js0 = 0; js0 < J; js0 += S) {
+      // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
+      if (js0 > 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      const int js = js0 + s;
+      if (js >= J) continue;
       const int q = js % Q;
       const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
       const int item = active ? js * RS + gi : I - 1;

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Aggregate an ncu capture's per-SASS stall samples and executed instructions
-by CUDA source line (needs -lineinfo): python scripts/ncu_lines.py REP [TOP]"""
+by CUDA source line (needs -lineinfo): python scripts/ncu_lines.py REP [TOP] [STALL_COLUMN]"""
 import csv
 import io
 import subprocess
@@ -8,6 +8,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+col = sys.argv[3] if len(sys.argv) > 3 else None  # e.g. stall_no_inst: rank by that stall reason
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 agg = {}
@@ -30,7 +31,7 @@ for r in csv.reader(io.StringIO(out)):
         continue
     f = lambda i: float(r[i]) if r[i] not in ("", "-") else 0.0
     try:
-        sv, iv = f(4), f(7)
+        sv, iv = f(hdr.index(col) if col else 4), f(7)
     except ValueError:
         continue
     key = (fname, line, r[1].strip()[:90])

@@ -19,7 +19,7 @@ t = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 k0 = t[0]
 print("chunk markers (us from chunk-0 start): res0, [it: epoch-start, epoch-end, res+sync-end]")
 for ch in range(4):
-    row = t[ch * 16: ch * 16 + 14]
+    row = t[ch * 16: ch * 16 + 16]
     print(ch, [(v - k0) / 1000 if v else None for v in row])
 rows = t[64:].reshape(-1, 8)
 print("row: prod(wait-start, acquired, lu-start, lu-end) cons(wait-start, acquired, done) in us")
@@ -30,3 +30,16 @@ cons = rows[:, 6] - rows[:, 5]
 lu = rows[:, 3] - rows[:, 2]
 print("consumer solve us: median %.3f; producer LU us: median %.3f; producer load us: median %.3f" % (
     np.median(cons[cons > 0]) / 1000, np.median(lu[lu > 0]) / 1000, np.median((rows[:, 2] - rows[:, 1])[lu > 0]) / 1000))
+ncx = min(nc, nt)
+ctas = t[64 + 8 * ncx:].reshape(-1, 8)
+ctas = ctas[ctas[:, 0] > 0]
+if len(ctas):
+    z = ctas[:, 0].min()
+    rel = (ctas[:, :6] - z) / 1000
+    print("per-CTA (us from earliest chunk start): start res0 bar1 epoch-end res bar2 ; spread / percentiles")
+    for j, name in enumerate(["start", "res0", "bar1", "epoch_end", "res", "bar2"]):
+        col = rel[:, j]
+        print(f"  {name:9s} min {col.min():8.2f}  p50 {np.median(col):8.2f}  max {col.max():8.2f}")
+    d = rel[:, 1:6] - rel[:, 0:5]
+    for j, name in enumerate(["res0", "bar1-wait", "epoch", "res", "bar2-wait"]):
+        print(f"  dur {name:10s} min {d[:, j].min():8.2f}  p50 {np.median(d[:, j]):8.2f}  max {d[:, j].max():8.2f}")
