@@ -60,7 +60,7 @@ __device__ __forceinline__ int producer_of(int warp) {
 constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay below 16
 constexpr int kSmemCap = 224 * 1024;
 constexpr int kRoundBarrier = 15;
-constexpr bool kFwdRounds = false;  // producers only; ring barriers use 1 .. 2Q <= 14
+constexpr bool kFwdRounds = true;  // producers only; ring barriers use 1 .. 2Q <= 14
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -81,9 +81,11 @@ struct Rec {
   static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
 };
 
-// Per-group pivot-row buffer: two rows of N + 1 doubles (row, reciprocal of its pivot).
+// Per-group pivot-row buffer: two rows of N + 2 doubles (16-byte aligned halves).
 template <int N>
-constexpr int kPb = 2 * (N + 1);
+constexpr int kPbRow = N + 2;
+template <int N>
+constexpr int kPb = 2 * kPbRow<N>;
 
 struct Shape {
   int S, Ws, LT;       // producer sets, producer warps per set, lanes per tile
@@ -139,6 +141,42 @@ __device__ __forceinline__ double group_max_nonneg(double v, int base, int gl) {
   return v;
 }
 
+enum { kLuOk = 0, kLuSingular = 1, kLuCheckExact = 2 };
+
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+template <int G>
+__device__ __forceinline__ double group_min(double v, int base, int gl) {
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) v = fmin(v, __shfl_sync(0xffffffffu, v, rot_src<G>(base, gl, off)));
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ float group_max_f(float v, int base, int gl) {
+#pragma unroll
+  for (int off = 1; off < G; off <<= 1) v = fmax_nan(v, __shfl_sync(0xffffffffu, v, rot_src<G>(base, gl, off)));
+  return v;
+}
+
+// Owner lane publishes row c of the block (columns c .. N-1) to the group
+// buffer; pairs go as 16-byte stores (buf is 16-byte aligned).
+template <int N>
+__device__ __forceinline__ void publish_row(double* buf, const double (&v)[N], int c) {
+  if (c & 1) buf[c] = v[c];
+#pragma unroll
+  for (int j = (c + 1) & ~1; j < N; j += 2) {
+    if (j + 1 < N)
+      *reinterpret_cast<double2*>(buf + j) = make_double2(v[j], v[j + 1]);
+    else
+      buf[j] = v[j];
+  }
+}
+
 // Row moves through shared memory, 16-byte accesses when rows stay aligned.
 template <int N>
 __device__ __forceinline__ void store_row(double* dst, const double (&v)[N]) {
@@ -180,28 +218,27 @@ __device__ __forceinline__ void load_row(const double* src, double (&v)[N]) {
 // identical to the reference's (multiplier by the pivot reciprocal). The whole
 // warp must call this; pb is a kPb<N>-double group buffer.
 template <int N>
-__device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec) {
+__device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec) {
   constexpr int G = Geo<N>::G, R = Geo<N>::R;
-  double lm = 0.0;
+  // max |a| for the singularity threshold on the high words only (one float
+  // max per element; exact order for |a| < 2^1017, NaN-propagating so any
+  // inf/NaN/huge entry defers to the exact test)
+  float lmf = 0.0f;
 #pragma unroll
   for (int s = 0; s < R; ++s)
     if (gl + s * G < N)
 #pragma unroll
-      for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(a[s][j]));
+      for (int j = 0; j < N; ++j) lmf = fmax_nan(lmf, fabsf(__int_as_float(__double2hiint(a[s][j]))));
   int orig[R];
 #pragma unroll
   for (int s = 0; s < R; ++s) orig[s] = gl + s * G;
   bool swapped = false;  // group-uniform
-  double pmin = INFINITY;
   int* iscr = reinterpret_cast<int*>(rec + Rec<N>::PERM);  // row-source scratch until perm is stored
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    double* buf = pb + (c & 1) * (N + 1);
+    double* buf = pb + (c & 1) * kPbRow<N>;
     const int sc = c / G, lc = c % G;  // slot / lane of row c
-    if (gl == lc) {
-#pragma unroll
-      for (int j = c; j < N; ++j) buf[j] = a[sc][j];
-    }
+    if (gl == lc) publish_row<N>(buf, a[sc], c);
     __syncwarp();
     double piv = buf[c];
     bool beat = false;
@@ -210,7 +247,7 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
       if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) beat |= fabs(a[s][c]) > fabs(piv);
     if (__any_sync(0xffffffffu, beat)) {
       // the reference's scan (strict '>' from row c down) over |a(r, c)| staged in the idle half of pb
-      double* cand = pb + ((c + 1) & 1) * (N + 1);
+      double* cand = pb + ((c + 1) & 1) * kPbRow<N>;
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int r = gl + s * G;
@@ -244,15 +281,10 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
         }
       }
       swapped |= p != c;
-      if (gl == lc) {
-#pragma unroll
-        for (int j = c; j < N; ++j) buf[j] = a[sc][j];
-      }
+      if (gl == lc) publish_row<N>(buf, a[sc], c);
       __syncwarp();
       piv = buf[c];
     }
-    const double apiv = fabs(piv);
-    pmin = fmin(pmin, apiv);  // the singularity test is applied once at the end
     const double inv = rcp_nr(piv);
     if (gl == 0) rec[Rec<N>::RD + c] = inv;
 #pragma unroll
@@ -266,8 +298,6 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
       }
     }
   }
-  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
-  const bool ok = !(pmin < tiny || pmin == 0.0);
   __syncwarp();  // rec scratch reads done before the factors overwrite it
   int* perm = reinterpret_cast<int*>(rec + Rec<N>::PERM);
 #pragma unroll
@@ -279,15 +309,64 @@ __device__ inline bool lu_group(double (&a)[Geo<N>::R][N], int gl, int base, dou
     }
   }
   if (gl == 0) perm[N] = swapped ? 0 : 1;
-  return ok;
+  __syncwarp();
+  // singularity (|pivot| < 1e-14 max|a| or a zero pivot) from the stored U diagonal
+  double pmin = INFINITY;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int i = gl + s * G;
+    if (i < N) pmin = fmin(pmin, fabs(rec[i * N + i]));
+  }
+  pmin = group_min<G>(pmin, base, gl);
+  lmf = group_max_f<G>(lmf, base, gl);
+  if (pmin == 0.0) return kLuSingular;
+  if (lmf != lmf) return kLuCheckExact;
+  const double mhi = __hiloint2double(__float_as_int(lmf), 0);  // <= max|a| < mhi (1 + 2^-20)
+  const double lo = 1e-14 * mhi;
+  if (pmin < lo) return kLuSingular;
+  if (pmin >= lo * (1.0 + 0x1p-18)) return kLuOk;
+  return kLuCheckExact;  // within 2^-18 of the threshold: the caller decides on the exact max
 }
 
-// Build the block with `build(m)` (rows this lane holds) and factor it.
-template <int N, class Build>
-__device__ inline bool factor_block(const Build& build, int gl, int base, double* pb, double* rec) {
-  double m[Geo<N>::R][N];
-  build(m);
-  return lu_group<N>(m, gl, base, pb, rec);
+// Exact form of the singularity test (rare: huge/non-finite entries or a
+// pivot within 2^-18 of the threshold): `rows(m)` rebuilds the block's
+// entries (in any row/column order — the adjoint passes the untransposed
+// rows) for the exact max |a|; the pivots are read from the stored factors.
+template <int N, class Rows>
+__device__ inline bool lu_exact_check(const Rows& rows, const double* rec, int gl, int base) {
+  constexpr int G = Geo<N>::G, R = Geo<N>::R;
+  double m[R][N];
+  rows(m);
+  double lm = 0.0, pmin = INFINITY;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int i = gl + s * G;
+    if (i < N) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) lm = fmax(lm, fabs(m[s][j]));
+      pmin = fmin(pmin, fabs(rec[i * N + i]));
+    }
+  }
+  const double tiny = 1e-14 * group_max_nonneg<G>(lm, base, gl);
+  pmin = group_min<G>(pmin, base, gl);
+  return !(pmin < tiny || pmin == 0.0);
+}
+
+// Build the block with `build(m)` (rows this lane holds) and factor it;
+// `rows` rebuilds the entries for the rare exact singularity test.
+template <int N, class Build, class Rows>
+__device__ inline bool factor_block(const Build& build, const Rows& rows, int gl, int base, double* pb, double* rec) {
+  int st;
+  {
+    double m[Geo<N>::R][N];
+    build(m);
+    st = lu_group<N>(m, gl, base, pb, rec);
+  }
+  if (__any_sync(0xffffffffu, st == kLuCheckExact)) {
+    const bool ok = lu_exact_check<N>(rows, rec, gl, base);
+    if (st == kLuCheckExact) return ok;
+  }
+  return st == kLuOk;
 }
 
 // lu_solve_vec (linalg.cpp:46-60) from a record, one thread: v <- M^{-1} v.
@@ -580,7 +659,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         }
       };
       if (tr) tr[2] = globaltimer_ns();
-      if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0) {
+      if (!factor_block<N>(build, build, gl, gr.base, pb, rec) && active && gl == 0) {
         atomicMin(a.sing_key, (unsigned long long)k * nb + b);
         atomicOr(s_sing, 1u);
       }
@@ -791,7 +870,22 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         if (gl == 0) rec[Rec<N>::DT] = dt;
         __syncwarp();
       };
-      if (!factor_block<N>(build, gl, gr.base, pb, rec) && active && gl == 0)
+      // the entries of M^T without the transpose scratch (same values, rows of I - dt J)
+      auto rows = [&](double (&mt)[Gm::R][N]) {
+#pragma unroll
+        for (int q = 0; q < Gm::R; ++q) {
+          const int i = gl + q * Gm::G;
+          if (i < N) {
+            MS::jac_row(a.m, cs, t, y, i, mt[q], b);
+#pragma unroll
+            for (int j = 0; j < N; ++j) mt[q][j] = (j == i) ? 1.0 - dt * mt[q][j] : -dt * mt[q][j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+          }
+        }
+      };
+      if (!factor_block<N>(build, rows, gl, gr.base, pb, rec) && active && gl == 0)
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + q, nthr);
     }
