@@ -116,3 +116,32 @@ def test_v2_divergence_payload(port):
         api.integrate_backward_euler(m, y0, api.TimeGrid(t), 30, api.NewtonSettings(1e-14, 1e-16, 1), ctx=ctx)
     g, w = got.value, want.value
     assert (g.chunk_start_step, g.batch_index, g.iterations) == (w.chunk_start_step, w.batch_index, w.iterations)
+
+
+@pytest.mark.parametrize("k", [-40, -9, -3, -1, 0, 1, 3, 9, 40])
+def test_singularity_threshold_band(port, k):
+    """Pivots straddling 1e-14 max|M| within the 2^-18 band where the kernels' high-word maximum defers to the
+    exact test: M = I - dt A upper triangular (no elimination rounding), max|M| = |m_01| with low-word bits set,
+    pivot m_22 = tiny (1 + k 2^-30). Singular or not, and where, must match the oracle."""
+    m01 = 1e6 * (1.0 + 2.0 ** -40)
+    tiny = 1e-14 * m01
+    a22 = 1.0 - tiny * (1.0 + k * 2.0 ** -30)  # dt = 1: m_22 = 1 - a22 (exact, Sterbenz)
+    p = np.array([0.0, -m01, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, a22, 1.0])
+    nb, nt = 3, 6
+    m = P.build_lin3(nb).with_params(p)
+    y0 = np.zeros((nb, 3))
+    t = uniform_times(nt, nb, float(nt))
+    try:
+        want = port.forward(m, y0, t, 2)
+        werr = None
+    except P.SingularBlock as e:
+        want, werr = None, e
+    ctx = _ctx(2)
+    if werr is not None:
+        with pytest.raises(P.SingularBlock) as got:
+            api.integrate_backward_euler(m, y0, api.TimeGrid(t), 2, ctx=ctx)
+        assert (got.value.chunk_index, got.value.batch_index) == (werr.chunk_index, werr.batch_index)
+    else:
+        got = api.integrate_backward_euler(m, y0, api.TimeGrid(t), 2, ctx=ctx)
+        assert rel_max(got.states, want.states) <= TOL
+    assert ctx.kernel_generation_used() == 2
