@@ -22,14 +22,41 @@ namespace v2 {
 template <int NU>
 struct MdsS {
   static constexpr int N = 2 * NU;
-  static constexpr int NCONST = 2 * NU + 1;
-  // cs[u] = K_u / M_u, cs[NU + u] = C_u / M_u, cs[2 NU] = f_a
+  // The Jacobian depends on neither the state, the time nor the lane
+  // (models_mds.cpp:54-82: entries are parameter ratios), so the kernels keep
+  // it in shared memory: J (row-major), J^T, and two shifted copies of a unit
+  // vector whose slices are the rows of I written as 1 / -0.0 (adding -0.0
+  // leaves every off-diagonal product bit-identical).
+  static constexpr bool kConstJac = true;
+  static constexpr int JOFF = ((2 * NU + 1) + 1) / 2 * 2;
+  static constexpr int JTOFF = JOFF + N * N;
+  static constexpr int ZOFF = JTOFF + N * N;
+  static constexpr int NCONST = ZOFF + 4 * N;
+  // cs[u] = K_u / M_u, cs[NU + u] = C_u / M_u, cs[2 NU] = f_a, then J, J^T, Z
   __device__ static void load_consts(const DevModel& m, double* cs) {
     for (int u = threadIdx.x; u < NU; u += blockDim.x) {
       cs[u] = m.p[u] / m.p[2 * NU + u];
       cs[NU + u] = m.p[NU + u] / m.p[2 * NU + u];
     }
     if (threadIdx.x == 0) cs[2 * NU] = m.p[3 * NU];
+    __syncthreads();
+    for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+      const int i = e / N, j = e % N;
+      double row[N], y[N] = {};
+      jac_row(m, cs, 0.0, y, i, row, 0);
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) v = q == j ? row[q] : v;
+      cs[JOFF + e] = v;
+      cs[JTOFF + j * N + i] = v;
+    }
+    for (int e = threadIdx.x; e < 4 * N; e += blockDim.x)
+      cs[ZOFF + e] = (e == N - 1 || e == 2 * N + N) ? 1.0 : -0.0;
+  }
+  // row i of I (1 on the diagonal, -0.0 elsewhere), 16-byte aligned
+  __device__ static const double* unit_row(const double* cs, int i) {
+    const int s = N - 1 - i;
+    return cs + ZOFF + ((s & 1) ? 2 * N + s + 1 : s);
   }
   __device__ static void rate(const DevModel& m, const double* cs, double t, const double (&y)[N], double (&h)[N],
                               int b) {

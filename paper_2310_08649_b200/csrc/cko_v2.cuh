@@ -16,6 +16,8 @@
 //  * the forward's all-lanes convergence predicate (integrate.cpp:176-182)
 //    stays the only cross-CTA coupling (grid_reduce_or, cko_common.cuh).
 #pragma once
+
+#include <type_traits>
 #include <cfloat>
 #include <climits>
 
@@ -59,8 +61,11 @@ __device__ __forceinline__ int producer_of(int warp) {
 }
 constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay below 16
 constexpr int kSmemCap = 224 * 1024;
-constexpr int kRoundBarrier = 15;
-constexpr bool kFwdRounds = true;  // producers only; ring barriers use 1 .. 2Q <= 14
+constexpr int kRoundBarrier = 15;  // producers only; ring barriers use 1 .. 2Q <= 14
+constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruction-cache locality)
+// The forward builds M from the model's per-entry selects (ALU) rather than
+// the shared-memory J rows: its LU already loads the shared-memory pipe.
+constexpr bool kFwdSharedJac = false;
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -79,6 +84,16 @@ struct Rec {
   static constexpr int PERM = DT + 1;                       // ints start here (as double offset)
   static constexpr int RAW = PERM + (N + 2) / 2;
   static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
+};
+
+// Models whose Jacobian is a per-CTA constant in shared memory (MdsS).
+template <class MS, class = void>
+struct HasConstJac {
+  static constexpr bool value = false;
+};
+template <class MS>
+struct HasConstJac<MS, std::void_t<decltype(MS::kConstJac)>> {
+  static constexpr bool value = MS::kConstJac;
 };
 
 // Per-group pivot-row buffer: two rows of N + 2 doubles (16-byte aligned halves).
@@ -644,11 +659,18 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         for (int q = 0; q < Gm::R; ++q) {
           const int i = gl + q * Gm::G;
           if (i < N) {
-            MS::jac_row(a.m, cs, t, y, i, m[q], b);
+            if constexpr (kFwdSharedJac && HasConstJac<MS>::value) {  // M = -dt J + I from shared memory
+              const double* Jr = cs + MS::JOFF + i * N;
+              const double* Er = MS::unit_row(cs, i);
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-              m[q][j] = xmul(ndt, m[q][j]);
-              if (j == i) m[q][j] = xadd(m[q][j], 1.0);
+              for (int j = 0; j < N; ++j) m[q][j] = xadd(xmul(ndt, Jr[j]), Er[j]);
+            } else {
+              MS::jac_row(a.m, cs, t, y, i, m[q], b);
+#pragma unroll
+              for (int j = 0; j < N; ++j) {
+                m[q][j] = xmul(ndt, m[q][j]);
+                if (j == i) m[q][j] = xadd(m[q][j], 1.0);
+              }
             }
             rec[Rec<N>::Y + i] = a.states[(size_t)(x.step + 1 + k) * x.row + (size_t)b * N + i];
             rec[Rec<N>::RHS + i] = r[i];
@@ -837,6 +859,32 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       load_vec<N>(a.states + (size_t)m * row + (size_t)b * N, y);
       // J rows into the record (scratch), then read back transposed
       auto build = [&](double (&mt)[Gm::R][N]) {
+        if constexpr (HasConstJac<MS>::value) {  // J^T rows straight from shared memory
+          const double ndt = -dt;
+#pragma unroll
+          for (int q = 0; q < Gm::R; ++q) {
+            const int i = gl + q * Gm::G;
+            if (i < N) {
+              const double* JTr = cs + MS::JTOFF + i * N;  // J[j][i], j = 0 .. N-1
+              const double* Er = MS::unit_row(cs, i);
+              double tmp = 0.0;  // (J^T lambda)_i (gemv_transpose)
+#pragma unroll
+              for (int j = 0; j < N; ++j) {
+                const double x = JTr[j];
+                tmp += x * lm[j];
+                mt[q][j] = xadd(xmul(ndt, x), Er[j]);
+              }
+              const double yi = a.states[(size_t)m * row + (size_t)b * N + i];
+              const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? yi / Lval : 0.0);
+              rec[Rec<N>::RHS + i] = dl + dt * tmp;
+            } else {
+#pragma unroll
+              for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+            }
+          }
+          if (gl == 0) rec[Rec<N>::DT] = dt;
+          return;
+        }
 #pragma unroll
         for (int q = 0; q < Gm::R; ++q) {
           const int i = gl + q * Gm::G;
@@ -885,7 +933,12 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
           }
         }
       };
-      if (!factor_block<N>(build, rows, gl, gr.base, pb, rec) && active && gl == 0)
+      bool fok;
+      if constexpr (HasConstJac<MS>::value)
+        fok = factor_block<N>(build, build, gl, gr.base, pb, rec);  // build leaves the factors alone
+      else
+        fok = factor_block<N>(build, rows, gl, gr.base, pb, rec);
+      if (!fok && active && gl == 0)
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + q, nthr);
     }
@@ -980,7 +1033,7 @@ inline Shape make_shape(int L) {
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
   for (sh.Q = 2 * sh.S;; sh.Q = sh.S) {
     // a tile row must never need a slot more than Q - 1 slots past the oldest unreleased one
-    sh.LT = min(32, (sh.Q - 1) * sh.RS);
+    sh.LT = min(min(32, L), (sh.Q - 1) * sh.RS);  // no wider than the CTA's lanes (shared memory)
     smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
     if (sh.Q == sh.S || (sh.Q <= kMaxSlots && tot * 8 <= kSmemCap)) break;
   }
