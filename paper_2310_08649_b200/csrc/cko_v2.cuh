@@ -232,7 +232,7 @@ __device__ __forceinline__ void load_row(const double* src, double (&v)[N]) {
 // each row's source row for the permutation. Arithmetic per column is then
 // identical to the reference's (multiplier by the pivot reciprocal). The whole
 // warp must call this; pb is a kPb<N>-double group buffer.
-template <int N>
+template <int N, bool kPred = false>
 __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, double* pb, double* rec) {
   constexpr int G = Geo<N>::G, R = Geo<N>::R;
   // max |a| for the singularity threshold on the high words only (one float
@@ -304,8 +304,18 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
     if (gl == 0) rec[Rec<N>::RD + c] = inv;
 #pragma unroll
     for (int s = 0; s < R; ++s) {
-      // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1
-      if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) {
+      // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1.
+      // kPred: predicated, not branched — rows on or above the pivot run the update with l = 0,
+      // which leaves them unchanged (up to the sign of a zero entry). Measured per kernel.
+      if constexpr (kPred) {
+        if (s * G + G - 1 > c) {
+          const bool below = gl + s * G > c && gl + s * G < N;
+          const double l = below ? a[s][c] * inv : 0.0;
+          if (below) a[s][c] = l;
+#pragma unroll
+          for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+        }
+      } else if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) {
         const double l = a[s][c] * inv;
         a[s][c] = l;
 #pragma unroll
@@ -369,13 +379,13 @@ __device__ inline bool lu_exact_check(const Rows& rows, const double* rec, int g
 
 // Build the block with `build(m)` (rows this lane holds) and factor it;
 // `rows` rebuilds the entries for the rare exact singularity test.
-template <int N, class Build, class Rows>
+template <int N, bool kPred = false, class Build, class Rows>
 __device__ inline bool factor_block(const Build& build, const Rows& rows, int gl, int base, double* pb, double* rec) {
   int st;
   {
     double m[Geo<N>::R][N];
     build(m);
-    st = lu_group<N>(m, gl, base, pb, rec);
+    st = lu_group<N, kPred>(m, gl, base, pb, rec);
   }
   if (__any_sync(0xffffffffu, st == kLuCheckExact)) {
     const bool ok = lu_exact_check<N>(rows, rec, gl, base);
@@ -935,9 +945,9 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       };
       bool fok;
       if constexpr (HasConstJac<MS>::value)
-        fok = factor_block<N>(build, build, gl, gr.base, pb, rec);  // build leaves the factors alone
+        fok = factor_block<N, true>(build, build, gl, gr.base, pb, rec);  // build leaves the factors alone
       else
-        fok = factor_block<N>(build, rows, gl, gr.base, pb, rec);
+        fok = factor_block<N, true>(build, rows, gl, gr.base, pb, rec);
       if (!fok && active && gl == 0)
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + q, nthr);
