@@ -271,7 +271,7 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
       __syncwarp();
       int p = c;
       double bv = cand[c];
-#pragma unroll 1
+#pragma unroll 4
       for (int r = c + 1; r < N; ++r) {
         const double v = cand[r];
         if (v > bv) bv = v, p = r;
