@@ -12,7 +12,8 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchunkode_b200.so")
+# CKO_LIB_PATH: an alternative build of the same library (kernel A/B experiments, scripts/build_variant.sh)
+LIB_PATH = os.environ.get("CKO_LIB_PATH") or os.path.join(HERE, "libchunkode_b200.so")
 
 _lib = None
 

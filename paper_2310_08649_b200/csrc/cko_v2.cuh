@@ -33,7 +33,10 @@ namespace v2 {
 // same values and write the same addresses, which keeps the warp converged.
 template <int N>
 struct Geo {
-  static constexpr int G = N <= 8 ? 1 : (N <= 16 ? 8 : (N <= 20 ? 10 : 16));
+#ifndef CKO_G20
+#define CKO_G20 10
+#endif
+  static constexpr int G = N <= 8 ? 1 : (N <= 16 ? 8 : (N <= 20 ? CKO_G20 : 16));
   static constexpr int R = (N + G - 1) / G;
   static constexpr int GPW = 32 / G;
 };
@@ -63,6 +66,10 @@ constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay be
 constexpr int kSmemCap = 224 * 1024;
 constexpr int kRoundBarrier = 15;  // producers only; ring barriers use 1 .. 2Q <= 14
 constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruction-cache locality)
+#ifndef CKO_ROUND_EVERY
+#define CKO_ROUND_EVERY 1
+#endif
+constexpr int kRoundEvery = CKO_ROUND_EVERY;  // rounds between producer barriers
 // The forward builds M from the model's per-entry selects (ALU) rather than
 // the shared-memory J rows: its LU already loads the shared-memory pipe.
 constexpr bool kFwdSharedJac = false;
@@ -403,7 +410,10 @@ __device__ inline bool factor_block(const Build& build, const Rows& rows, int gl
 // j-ascending sum). vs: this thread's N-double scratch for the permuted gather.
 template <int N>
 __device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* vs, double (&v)[N]) {
-  constexpr int B = 4;
+#ifndef CKO_SOLVE_B
+#define CKO_SOLVE_B 4
+#endif
+  constexpr int B = CKO_SOLVE_B;
   const double* rec = static_cast<const double*>(__builtin_assume_aligned(rec_in, 16));
   const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
   double y[N];
@@ -646,7 +656,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
     unsigned long long* tr0 = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
     for (int js0 = 0; js0 < J; js0 += S) {
       // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
-      if (kFwdRounds && js0 > 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      if (kFwdRounds && js0 > 0 && (js0 / S) % kRoundEvery == 0) bar_sync(kRoundBarrier, 32 * S * Ws);
       const int js = js0 + s;
       if (js >= J) continue;
       const int q = js % Q;
@@ -851,7 +861,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
     for (int js0 = 0; js0 < J; js0 += S) {
       // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
-      if (js0 > 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      if (js0 > 0 && (js0 / S) % kRoundEvery == 0) bar_sync(kRoundBarrier, 32 * S * Ws);
       const int js = js0 + s;
       if (js >= J) continue;
       const int q = js % Q;
@@ -893,40 +903,40 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
             }
           }
           if (gl == 0) rec[Rec<N>::DT] = dt;
-          return;
-        }
+        } else {
 #pragma unroll
-        for (int q = 0; q < Gm::R; ++q) {
-          const int i = gl + q * Gm::G;
-          if (i < N) {
-            double jr[N];
-            MS::jac_row(a.m, cs, t, y, i, jr, b);
+          for (int q = 0; q < Gm::R; ++q) {
+            const int i = gl + q * Gm::G;
+            if (i < N) {
+              double jr[N];
+              MS::jac_row(a.m, cs, t, y, i, jr, b);
 #pragma unroll
-            for (int j = 0; j < N; ++j) rec[i * N + j] = jr[j];
+              for (int j = 0; j < N; ++j) rec[i * N + j] = jr[j];
+            }
           }
-        }
-        __syncwarp();
+          __syncwarp();
 #pragma unroll
-        for (int q = 0; q < Gm::R; ++q) {
-          const int i = gl + q * Gm::G;
-          if (i < N) {
+          for (int q = 0; q < Gm::R; ++q) {
+            const int i = gl + q * Gm::G;
+            if (i < N) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) mt[q][j] = rec[j * N + i];  // J[j][i]
-            double tmp = 0.0;                                      // (J^T lambda)_i (gemv_transpose)
+              for (int j = 0; j < N; ++j) mt[q][j] = rec[j * N + i];  // J[j][i]
+              double tmp = 0.0;                                      // (J^T lambda)_i (gemv_transpose)
 #pragma unroll
-            for (int j = 0; j < N; ++j) tmp += mt[q][j] * lm[j];
-            const double yi = a.states[(size_t)m * row + (size_t)b * N + i];
-            const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? yi / Lval : 0.0);
-            rec[Rec<N>::RHS + i] = dl + dt * tmp;
+              for (int j = 0; j < N; ++j) tmp += mt[q][j] * lm[j];
+              const double yi = a.states[(size_t)m * row + (size_t)b * N + i];
+              const double dl = a.dL ? a.dL[(size_t)m * row + (size_t)b * N + i] : (Lval > 0.0 ? yi / Lval : 0.0);
+              rec[Rec<N>::RHS + i] = dl + dt * tmp;
 #pragma unroll
-            for (int j = 0; j < N; ++j) mt[q][j] = (j == i) ? 1.0 - dt * mt[q][j] : -dt * mt[q][j];
-          } else {
+              for (int j = 0; j < N; ++j) mt[q][j] = (j == i) ? 1.0 - dt * mt[q][j] : -dt * mt[q][j];
+            } else {
 #pragma unroll
-            for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+              for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+            }
           }
+          if (gl == 0) rec[Rec<N>::DT] = dt;
+          __syncwarp();
         }
-        if (gl == 0) rec[Rec<N>::DT] = dt;
-        __syncwarp();
       };
       // the entries of M^T without the transpose scratch (same values, rows of I - dt J)
       auto rows = [&](double (&mt)[Gm::R][N]) {
