@@ -417,13 +417,35 @@ cko_status check_lanes(const cko_model* m, int nb, cko_error* err) {
   return CKO_OK;
 }
 
-cko_status check_grid_host(const double* times, int nt, int nb, cko_error* err) {
+cko_status check_grid_shape(int nt, int nb, cko_error* err) {
   if (nt < 1 || nb < 1)
     return fail(err, CKO_INVALID_TIME_GRID, "time grid needs at least one step and one batch lane");
-  for (int i = 1; i <= nt; ++i)
-    for (int b = 0; b < nb; ++b)
-      if (!(times[(size_t)i * nb + b] > times[(size_t)(i - 1) * nb + b]))
-        return fail(err, CKO_INVALID_TIME_GRID, "time grid must be strictly increasing (step %d, batch %d)", i, b);
+  return CKO_OK;
+}
+
+// TimeGrid validation (time_grid.cpp:7-19) on the device copy: the first
+// non-increasing entry in the reference's scan order (step, then lane).
+__global__ void grid_check_kernel(const double* __restrict__ t, long long total, int nb,
+                                  unsigned long long* __restrict__ key) {
+  for (long long e = nb + (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    if (!(t[e] > t[e - nb])) atomicMin(key, (unsigned long long)e);
+}
+
+cko_status check_grid_device(cko_ctx* c, const double* d_times, int nt, int nb, cko_error* err) {
+  CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(c->pin.ensure(64));
+  CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+  const long long total = (long long)nb * (nt + 1);
+  grid_check_kernel<<<4 * c->sms, 256, 0, c->stream>>>(d_times, total, nb, c->key.as<unsigned long long>());
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long* h = c->pin.as<unsigned long long>(48);
+  CUDA_TRY(cudaMemcpyAsync(h, c->key.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (*h != ~0ull) {
+    const int i = (int)(*h / (unsigned long long)nb), b = (int)(*h % (unsigned long long)nb);
+    return fail(err, CKO_INVALID_TIME_GRID, "time grid must be strictly increasing (step %d, batch %d)", i, b);
+  }
   return CKO_OK;
 }
 
@@ -773,7 +795,7 @@ cko_status cko_be_forward(cko_ctx* c, const cko_model* m, const double* y0, cons
                           cko_traj** traj_out, cko_work* work, cko_error* err) {
   if (!c || !m || !y0 || !times || !st || !sv) return fail(err, CKO_ERROR, "null argument");
   if (traj_out) *traj_out = nullptr;
-  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  if (cko_status s = check_grid_shape(nt, nb, err)) return s;
   CUDA_TRY(cudaSetDevice(c->device));
   const int n = m->dm.n;
   const size_t row = (size_t)nb * n;
@@ -815,6 +837,7 @@ cko_status cko_be_forward(cko_ctx* c, const cko_model* m, const double* y0, cons
                                   c->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) return cleanup(fail(err, CKO_CUDA, "H2D: %s", cudaGetErrorString(e)));
+  if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return cleanup(s);
   cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, work, nullptr, err);
   if (s != CKO_OK) return cleanup(s);
   if (states_out) {
@@ -858,7 +881,7 @@ cko_status cko_be_adjoint_host(cko_ctx* c, const cko_model* m, const double* sta
                                int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* dL_host,
                                double* loss_out, double* grad_out, cko_work* bwd, cko_error* err) {
   if (!c || !m || !states || !times || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
-  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  if (cko_status s = check_grid_shape(nt, nb, err)) return s;
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t row = (size_t)nb * m->dm.n;
   CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
@@ -866,6 +889,7 @@ cko_status cko_be_adjoint_host(cko_ctx* c, const cko_model* m, const double* sta
   CUDA_TRY(cudaMemcpyAsync(c->h_states.p, states, sizeof(double) * row * (nt + 1), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice,
                            c->stream));
+  if (cko_status s = check_grid_device(c, c->h_times.as<double>(), nt, nb, err)) return s;
   const double* d_dL = nullptr;
   if (loss_kind == CKO_LOSS_USER) {
     if (!dL_host) return fail(err, CKO_ERROR, "user loss needs dL");
@@ -882,7 +906,7 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
                                 double* states_out, double* loss_out, double* grad_out, cko_work* fwd, cko_work* bwd,
                                 cko_error* err) {
   if (!c || !m || !y0 || !times || !st || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
-  if (cko_status s = check_grid_host(times, nt, nb, err)) return s;
+  if (cko_status s = check_grid_shape(nt, nb, err)) return s;
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t row = (size_t)nb * m->dm.n;
   CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
@@ -891,6 +915,7 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
   double* d_times = c->h_times.as<double>();
   CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
+  if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
   if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err)) return s;
   if (states_out) {
     CUDA_TRY(cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost,

@@ -199,3 +199,36 @@ def test_linear_counter_laws():
     assert tr.work.newton_iterations == 2
     assert tr.work.linear_solves == tr.work.newton_iterations
     assert tr.work.rate_evals == tr.work.newton_iterations + 2
+
+
+@pytest.mark.parametrize("entry", ["forward", "gradient"])
+def test_time_grid_checked_on_device(entry):
+    """The C ABI validates host grids after the copy (time_grid.cpp:7-19) and names the first non-increasing
+    entry in the reference's scan order; the Python TimeGrid never gets here, so call the ABI directly."""
+    import ctypes as C
+
+    from paper_2310_08649_b200 import abi
+    from paper_2310_08649_b200._native import lib
+    from paper_2310_08649_b200.errors import raise_for
+
+    nb, nt, n = 5, 40, 3
+    m = P.build_lin3(nb)
+    t = uniform_times(nt, nb, 1.0)
+    t[17, 3] = t[16, 3]  # first violation in (step, lane) order ...
+    t[30, 1] = t[29, 1] - 1.0  # ... not this later one
+    t = np.ascontiguousarray(t)
+    y0 = np.zeros((nb, n))
+    ctx = api.Context(0)
+    st, sv, w, w2, e = api.NewtonSettings().c(), api.SolverChoice().c(), abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    states = np.zeros((nt + 1, nb * n))
+    if entry == "forward":
+        rc = lib().cko_be_forward(ctx.h, ctx.model(m), dp(y0), dp(t), nb, nt, 4, C.byref(st), C.byref(sv), dp(states),
+                                  None, C.byref(w), C.byref(e))
+    else:
+        loss, grad = C.c_double(), np.zeros(m.params.size)
+        rc = lib().cko_gradient_adjoint(ctx.h, ctx.model(m), dp(y0), dp(t), nb, nt, 4, C.byref(st), C.byref(sv),
+                                        None, C.byref(loss), dp(grad), C.byref(w), C.byref(w2), C.byref(e))
+    assert rc == abi.CKO_INVALID_TIME_GRID
+    with pytest.raises(P.InvalidTimeGrid, match=r"step 17, batch 3"):
+        raise_for(rc, e)
