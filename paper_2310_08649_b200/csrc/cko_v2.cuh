@@ -70,6 +70,10 @@ constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruct
 #define CKO_ROUND_EVERY 1
 #endif
 constexpr int kRoundEvery = CKO_ROUND_EVERY;  // rounds between producer barriers
+#ifndef CKO_LOOKAHEAD
+#define CKO_LOOKAHEAD 0
+#endif
+constexpr bool kLookahead = CKO_LOOKAHEAD;  // group LU publishes row c + 1 during column c
 // The forward builds M from the model's per-entry selects (ALU) rather than
 // the shared-memory J rows: its LU already loads the shared-memory pipe.
 constexpr bool kFwdSharedJac = false;
@@ -260,7 +264,7 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
   for (int c = 0; c < N; ++c) {
     double* buf = pb + (c & 1) * kPbRow<N>;
     const int sc = c / G, lc = c % G;  // slot / lane of row c
-    if (gl == lc) publish_row<N>(buf, a[sc], c);
+    if ((!kLookahead || c == 0) && gl == lc) publish_row<N>(buf, a[sc], c);
     __syncwarp();
     double piv = buf[c];
     bool beat = false;
@@ -309,11 +313,10 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
     }
     const double inv = rcp_nr(piv);
     if (gl == 0) rec[Rec<N>::RD + c] = inv;
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1.
-      // kPred: predicated, not branched — rows on or above the pivot run the update with l = 0,
-      // which leaves them unchanged (up to the sign of a zero entry). Measured per kernel.
+    // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1.
+    // kPred: predicated, not branched — rows on or above the pivot run the update with l = 0,
+    // which leaves them unchanged (up to the sign of a zero entry). Measured per kernel.
+    auto update = [&](int s) {
       if constexpr (kPred) {
         if (s * G + G - 1 > c) {
           const bool below = gl + s * G > c && gl + s * G < N;
@@ -328,6 +331,19 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
 #pragma unroll
         for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
       }
+    };
+    if (kLookahead && c + 1 < N) {
+      // look-ahead: the slot holding row c + 1 first, its owner publishes it for the next
+      // column while the other slot updates
+      const int sn = (c + 1) / G;
+      update(sn);
+      if (gl == (c + 1) % G) publish_row<N>(pb + ((c + 1) & 1) * kPbRow<N>, a[sn], c + 1);
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        if (s != sn) update(s);
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) update(s);
     }
   }
   __syncwarp();  // rec scratch reads done before the factors overwrite it
