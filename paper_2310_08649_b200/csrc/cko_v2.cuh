@@ -66,6 +66,9 @@ constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay be
 constexpr int kSmemCap = 224 * 1024;
 constexpr int kRoundBarrier = 15;  // producers only; ring barriers use 1 .. 2Q <= 14
 constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruction-cache locality)
+#ifndef CKO_ROUND_PER_SMSP
+#define CKO_ROUND_PER_SMSP 1
+#endif
 #ifndef CKO_ROUND_EVERY
 #define CKO_ROUND_EVERY 1
 #endif
@@ -138,6 +141,15 @@ __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+
+// round barrier: all producer warps (15), or per SMSP (13 .. 15, three producer warps each)
+__device__ __forceinline__ void producer_round_sync(int warp, int nprod) {
+  if (CKO_ROUND_PER_SMSP && nprod == 9)
+    bar_sync(12 + (warp & 3), 96);
+  else
+    bar_sync(15, 32 * nprod);
+}
+
 
 // 1 / x to within an ulp: the hardware seed refined by two Newton steps (no
 // special-case path; pivots here are finite and nonzero or the block is
@@ -672,7 +684,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
     unsigned long long* tr0 = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
     for (int js0 = 0; js0 < J; js0 += S) {
       // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
-      if (kFwdRounds && js0 > 0 && (js0 / S) % kRoundEvery == 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      if (kFwdRounds && js0 > 0 && (js0 / S) % kRoundEvery == 0) producer_round_sync(warp, S * Ws);
       const int js = js0 + s;
       if (js >= J) continue;
       const int q = js % Q;
@@ -877,7 +889,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     double* pb = pbs + (size_t)(s * RS + gi) * kPb<N>;
     for (int js0 = 0; js0 < J; js0 += S) {
       // the sets advance in rounds: producer warps stay at nearby code (instruction-cache locality)
-      if (js0 > 0 && (js0 / S) % kRoundEvery == 0) bar_sync(kRoundBarrier, 32 * S * Ws);
+      if (js0 > 0 && (js0 / S) % kRoundEvery == 0) producer_round_sync(warp, S * Ws);
       const int js = js0 + s;
       if (js >= J) continue;
       const int q = js % Q;
