@@ -79,7 +79,14 @@ constexpr int kRoundEvery = CKO_ROUND_EVERY;  // rounds between producer barrier
 constexpr bool kLookahead = CKO_LOOKAHEAD;  // group LU publishes row c + 1 during column c
 // The forward builds M from the model's per-entry selects (ALU) rather than
 // the shared-memory J rows: its LU already loads the shared-memory pipe.
-constexpr bool kFwdSharedJac = false;
+#ifndef CKO_FWD_SHARED_JAC
+#define CKO_FWD_SHARED_JAC 0
+#endif
+constexpr bool kFwdSharedJac = CKO_FWD_SHARED_JAC;
+#ifndef CKO_FWD_PRED
+#define CKO_FWD_PRED 0
+#endif
+constexpr bool kFwdPred = CKO_FWD_PRED;  // predicated trailing update in the forward LU
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -729,7 +736,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         }
       };
       if (tr) tr[2] = globaltimer_ns();
-      if (!factor_block<N>(build, build, gl, gr.base, pb, rec) && active && gl == 0) {
+      if (!factor_block<N, kFwdPred>(build, build, gl, gr.base, pb, rec) && active && gl == 0) {
         atomicMin(a.sing_key, (unsigned long long)k * nb + b);
         atomicOr(s_sing, 1u);
       }
