@@ -567,7 +567,11 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
     nrm = stage + cap - P;
     cap -= P;
   }
-  const int KB = cap > LN + L ? (cap - LN - L) / (2 * LN + L) : 0;  // rows per staged block
+  // lanes per staged tile: all of them when at least 4 rows fit, else fewer (wide CTAs)
+  int Lt = L;
+  if (cap < 9 * LN + 9 * L) Lt = max(1, min(L, cap / (9 * (N + 1))));
+  const int LtN = Lt * N;
+  const int KB = cap > LtN + Lt ? (cap - LtN - Lt) / (2 * LtN + Lt) : 0;  // rows per staged block
   if (KB < 1) {  // no room to stage: one point per thread straight from L2
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       const int k = p / L, lb = p % L, b = x.lb0 + lb;
@@ -588,58 +592,68 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
       nrm[p] = s;
     }
   }
-  for (int k0 = 0; KB >= 1 && k0 < x.c; k0 += KB) {
-    const int kb = min(KB, x.c - k0);
-    double* Y = stage;              // trajectory rows step + k0 .. step + k0 + kb
-    double* T = Y + (kb + 1) * LN;  // their times
-    double* O = T + (kb + 1) * L;   // residuals of rows k0 .. k0 + kb - 1
-    const double* src = a.states + (size_t)(x.step + k0) * x.row + (size_t)x.lb0 * N;
-    // asynchronous copies: every element in flight at once instead of one L2 round trip per element
-    {
-      // thread -> (row, 16-byte unit): several rows per pass, no divisions in the loop
-      constexpr int U = N % 2 == 0 ? 2 : 1;  // doubles per copy unit (rows stay 16-byte aligned for even N)
-      const int W = LN / U, rpp = blockDim.x >= W ? blockDim.x / W : 1;
-      const int r0 = threadIdx.x / W, e0 = threadIdx.x - r0 * W;
-      if (r0 < rpp)
-        for (int rr = r0; rr <= kb; rr += rpp)
-          for (int e = e0; e < W; e += blockDim.x) {
-            if constexpr (U == 2)
-              cp_async16(Y + rr * LN + 2 * e, src + (size_t)rr * x.row + 2 * e);
-            else
-              cp_async8(Y + rr * LN + e, src + (size_t)rr * x.row + e);
-          }
-    }
-    const double* ts = a.times + (size_t)(x.step + k0) * nb + x.lb0;
-    for (int e = threadIdx.x; e < (kb + 1) * L; e += blockDim.x) {
-      const int rr = e / L;
-      cp_async8(T + e, ts + (size_t)rr * nb + (e - rr * L));
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    if (rtr && k0 == 0) rtr[3] = globaltimer_ns();
-    for (int p = threadIdx.x; p < kb * L; p += blockDim.x) {
-      const int kk = p / L, lb = p - kk * L, b = x.lb0 + lb;
-      const double t = T[(kk + 1) * L + lb];
-      const double dt = t - T[kk * L + lb];
-      double y[N], ym[N], h[N];
-      load_vec<N>(Y + (kk + 1) * LN + lb * N, y);
-      load_vec<N>(Y + kk * LN + lb * N, ym);
-      MS::rate(a.m, cs, t, y, h, b);
-      double s = 0.0;
-      double* o = O + p * N;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
-        o[i] = v;
-        s = xadd(s, xmul(v, v));
+  for (int l0 = 0; KB >= 1 && l0 < L; l0 += Lt) {
+    const int Lc = min(Lt, L - l0), LcN = Lc * N;
+    for (int k0 = 0; k0 < x.c; k0 += KB) {
+      const int kb = min(KB, x.c - k0);
+      double* Y = stage;               // trajectory rows step + k0 .. step + k0 + kb, lanes l0 .. l0 + Lc
+      double* T = Y + (kb + 1) * LcN;  // their times
+      double* O = T + (kb + 1) * Lc;   // residuals of rows k0 .. k0 + kb - 1
+      const double* src = a.states + (size_t)(x.step + k0) * x.row + (size_t)(x.lb0 + l0) * N;
+      // asynchronous copies: every element in flight at once instead of one L2 round trip per element
+      {
+        // thread -> (row, 16-byte unit): several rows per pass, no divisions in the loop
+        constexpr int U = N % 2 == 0 ? 2 : 1;  // doubles per copy unit (rows stay 16-byte aligned for even N)
+        const int W = LcN / U, rpp = blockDim.x >= W ? blockDim.x / W : 1;
+        const int r0 = threadIdx.x / W, e0 = threadIdx.x - r0 * W;
+        if (r0 < rpp)
+          for (int rr = r0; rr <= kb; rr += rpp)
+            for (int e = e0; e < W; e += blockDim.x) {
+              if constexpr (U == 2)
+                cp_async16(Y + rr * LcN + 2 * e, src + (size_t)rr * x.row + 2 * e);
+              else
+                cp_async8(Y + rr * LcN + e, src + (size_t)rr * x.row + e);
+            }
       }
-      nrm[k0 * L + p] = s;
+      const double* ts = a.times + (size_t)(x.step + k0) * nb + x.lb0 + l0;
+      for (int e = threadIdx.x; e < (kb + 1) * Lc; e += blockDim.x) {
+        const int rr = e / Lc;
+        cp_async8(T + e, ts + (size_t)rr * nb + (e - rr * Lc));
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      if (rtr && k0 == 0 && l0 == 0) rtr[3] = globaltimer_ns();
+      for (int p = threadIdx.x; p < kb * Lc; p += blockDim.x) {
+        const int kk = p / Lc, lt = p - kk * Lc, lb = l0 + lt, b = x.lb0 + lb;
+        const double t = T[(kk + 1) * Lc + lt];
+        const double dt = t - T[kk * Lc + lt];
+        double y[N], ym[N], h[N];
+        load_vec<N>(Y + (kk + 1) * LcN + lt * N, y);
+        load_vec<N>(Y + kk * LcN + lt * N, ym);
+        MS::rate(a.m, cs, t, y, h, b);
+        double s = 0.0;
+        double* o = O + p * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
+          o[i] = v;
+          s = xadd(s, xmul(v, v));
+        }
+        nrm[(k0 + kk) * L + lb] = s;
+      }
+      __syncthreads();
+      if (rtr && k0 == 0 && l0 == 0) rtr[4] = globaltimer_ns();
+      if (Lc == L) {  // the block's residuals are one contiguous run of hr
+        double* dst = hr + (size_t)k0 * LN;
+        for (int e = threadIdx.x; e < kb * LN; e += blockDim.x) dst[e] = O[e];
+      } else {
+        for (int e = threadIdx.x; e < kb * LcN; e += blockDim.x) {
+          const int kk = e / LcN;
+          hr[((size_t)(k0 + kk) * L + l0) * N + (e - kk * LcN)] = O[e];
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    if (rtr && k0 == 0) rtr[4] = globaltimer_ns();
-    double* dst = hr + (size_t)k0 * LN;
-    for (int e = threadIdx.x; e < kb * LN; e += blockDim.x) dst[e] = O[e];
-    __syncthreads();
   }
   if (threadIdx.x == 0) *s_flags = 0;
   if (rtr) rtr[0] = globaltimer_ns();
