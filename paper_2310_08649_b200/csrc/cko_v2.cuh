@@ -69,6 +69,9 @@ constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruct
 #ifndef CKO_ROUND_PER_SMSP
 #define CKO_ROUND_PER_SMSP 1
 #endif
+#ifndef CKO_XCHG2
+#define CKO_XCHG2 2  // 0: all-rows swap through the record; 1: shuffle argmax + 2-lane swap; 2: scan + 2-lane swap
+#endif
 #ifndef CKO_ROUND_EVERY
 #define CKO_ROUND_EVERY 1
 #endif
@@ -291,6 +294,75 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
     for (int s = 0; s < R; ++s)
       if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) beat |= fabs(a[s][c]) > fabs(piv);
     if (__any_sync(0xffffffffu, beat)) {
+#if CKO_XCHG2
+#if CKO_XCHG2 == 2
+      // the reference's scan (strict '>' from row c down) over |a(r, c)| staged in the idle half of pb
+      double* cand = pb + ((c + 1) & 1) * kPbRow<N>;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + s * G;
+        if (s * G + G - 1 >= c && r >= c && r < N) cand[r] = fabs(a[s][c]);
+      }
+      __syncwarp();
+      int p = c;
+      double bv = cand[c];
+#pragma unroll 4
+      for (int r = c + 1; r < N; ++r) {
+        const double v = cand[r];
+        if (v > bv) bv = v, p = r;
+      }
+#else
+      // argmax over the group's rows r >= c by rotation shuffles (larger |a| wins, ties to the smaller
+      // r): the first maximum of the reference's strict '>' scan; a NaN pivot keeps row c like the scan
+      double bv = -1.0;
+      int br = INT_MAX;
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int r = gl + s * G;
+        if (s * G + G - 1 >= c && r >= c && r < N) {
+          const double v = fabs(a[s][c]);
+          if (v > bv) bv = v, br = r;  // slots ascend in r: '>' keeps the smaller r on ties
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < G; off <<= 1) {
+        const int src = rot_src<G>(base, gl, off);
+        const double ov = __shfl_sync(0xffffffffu, bv, src);
+        const int orr = __shfl_sync(0xffffffffu, br, src);
+        if (ov > bv || (ov == bv && orr < br)) bv = ov, br = orr;
+      }
+      const int p = (br == INT_MAX || !(fabs(piv) < bv)) ? c : br;
+#endif
+      // exchange rows c and p through two scratch rows at the front of the record (the factors are
+      // stored at the end); the owner(s) write both rows, then read them back swapped
+      const int sp = p / G, lp = p % G;
+      const bool cross = p != c;
+      if (cross && gl == lc) {
+        store_row<N>(rec, a[sc]);
+        iscr[0] = orig[sc];
+      }
+      if (cross && gl == lp) {
+#pragma unroll
+        for (int s = 0; s < R; ++s)
+          if (s == sp) {
+            store_row<N>(rec + N, a[s]);
+            iscr[1] = orig[s];
+          }
+      }
+      __syncwarp();
+      if (cross && gl == lc) {
+        load_row<N>(rec + N, a[sc]);
+        orig[sc] = iscr[1];
+      }
+      if (cross && gl == lp) {
+#pragma unroll
+        for (int s = 0; s < R; ++s)
+          if (s == sp) {
+            load_row<N>(rec, a[s]);
+            orig[s] = iscr[0];
+          }
+      }
+#else
       // the reference's scan (strict '>' from row c down) over |a(r, c)| staged in the idle half of pb
       double* cand = pb + ((c + 1) & 1) * kPbRow<N>;
 #pragma unroll
@@ -325,6 +397,7 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
           orig[s] = iscr[r];
         }
       }
+#endif
       swapped |= p != c;
       if (gl == lc) publish_row<N>(buf, a[sc], c);
       __syncwarp();
