@@ -145,3 +145,36 @@ def test_singularity_threshold_band(port, k):
         got = api.integrate_backward_euler(m, y0, api.TimeGrid(t), 2, ctx=ctx)
         assert rel_max(got.states, want.states) <= TOL
     assert ctx.kernel_generation_used() == 2
+
+
+@pytest.mark.parametrize("dt", [5e-6, 5e-5, 5e-4])
+def test_mds_pivot_heavy(port, dt):
+    """Larger steps: the reference's partial pivoting exchanges rows in most columns of the forward blocks
+    (same-lane and cross-lane pairs of the 10-lane groups) — factors, pivots and parity must hold."""
+    nb, nt = 9, 40
+    m = P.build_mass_damper_spring(10, nb)
+    rng = np.random.default_rng(11)
+    y0 = rng.uniform(-1e-3, 1e-3, (nb, 20))
+    t = uniform_times(nt, nb, nt * dt)
+    want = port.gradient(m, y0, t, 8)
+    ctx = _ctx(2)
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), 8, ctx=ctx)
+    assert ctx.kernel_generation_used() == 2
+    _check(got, want)
+
+
+def test_mds_cross_lane_exchanges(port):
+    """Alternating light / heavy masses: the pivot of column u is the velocity row of the NEXT unit, held by
+    another lane of the 10-lane group (cross-lane row exchange)."""
+    nb, nt = 7, 30
+    m = P.build_mass_damper_spring(10, nb)
+    p = np.array(m.params)
+    p[20:30] = [1e-3 if u % 2 == 0 else 1e-8 for u in range(10)]  # M_u
+    m = m.with_params(p)
+    y0 = np.zeros((nb, 20))
+    t = uniform_times(nt, nb, nt * 1e-6)
+    want = port.gradient(m, y0, t, 6)
+    ctx = _ctx(2)
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), 6, ctx=ctx)
+    assert ctx.kernel_generation_used() == 2
+    _check(got, want)
