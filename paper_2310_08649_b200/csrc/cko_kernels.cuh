@@ -113,6 +113,8 @@ size_t vjp_scratch_doubles(const DevModel& m, int nb, int nt);
 // VJP as split-K outer products (cko_node_vjp.cu).
 bool vjp_needs_outer(const DevModel& m);
 size_t node_vjp_scratch_doubles(const DevModel& m, int nb, int nt);
+cudaError_t launch_node_vectors_dmma(const DevModel& m, const double* states, const double* times, const double* wq,
+                                     int nb, size_t P, double* vec, cudaStream_t st);
 cudaError_t launch_node_vjp(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
                             int nt, double* scratch, double* grad, cudaStream_t st);
 cudaError_t launch_vjp(const DevModel& m, const double* states, const double* times,

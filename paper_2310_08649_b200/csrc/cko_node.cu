@@ -342,6 +342,151 @@ inline int blocks_for(size_t work, int threads) {
 
 }  // namespace node
 
+namespace node {
+
+// Per-point vectors of the parameter VJP (cko_node_vjp.cu, models_node.cpp:109-151)
+// for the C4 shape, 32 points per tile: z0, z1 = tanh(W1 z0 + b1),
+// z2 = tanh(W2 z1 + b2), o = tanh(W3 z2 + b3), d3 = w (1 - o^2),
+// d2 = (W3^T d3)(1 - z2^2), d1 = (W2^T d2)(1 - z1^2). The two 128 x 128 products
+// (W2 z1, W2^T d2) run as DMMA m8n8k4 (warp w: rows 16w .. 16w+15, 4 tile
+// columns, 32 k-steps); outputs feature-major x[f * P + p] like node_vectors_kernel.
+constexpr int TV = 32;                     // points per tile
+constexpr int kVecThreads = 256;
+constexpr int kVecSmem = (3 * W * TV + TV * W0 + N * TV) * 8;  // z1, X, d2 | z0 | d3
+
+__global__ void __launch_bounds__(kVecThreads) node_vectors_dmma_kernel(DevModel m, const double* states,
+                                                                        const double* times, const double* wq,
+                                                                        int nb, size_t P, double* vec) {
+  extern __shared__ __align__(16) double smem[];
+  double* sZ1 = smem;            // (W x TV)
+  double* sX = sZ1 + W * TV;     // (W x TV): W2 z1 + b2 -> z2
+  double* sD2 = sX + W * TV;     // (W x TV)
+  double* sZ0 = sD2 + W * TV;    // (TV x W0)
+  double* sD3 = sZ0 + TV * W0;   // (N x TV)
+  const Views v(m.p);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t row = (size_t)nb * N;
+  double* Z0 = vec;
+  double* Z1 = Z0 + (size_t)W0 * P;
+  double* Z2 = Z1 + (size_t)W * P;
+  double* D1 = Z2 + (size_t)W * P;
+  double* D2 = D1 + (size_t)W * P;
+  double* D3 = D2 + (size_t)W * P;
+  const size_t ntiles = (P + TV - 1) / TV;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t p0 = tile * TV;
+    // z0 = [y; sin(2 pi t / T_b)] of trajectory row mm = 1 + p / nb
+    for (int e = tid; e < TV * W0; e += blockDim.x) {
+      const int q = e / W0, i = e % W0;
+      const size_t p = min(p0 + q, P - 1);
+      const int mm = 1 + (int)(p / nb), b = (int)(p % nb);
+      const double z = i < N ? states[(size_t)mm * row + (size_t)b * N + i]
+                             : sin(CKO_TWO_PI * times[(size_t)mm * nb + b] / m.periods[m.off + b]);
+      sZ0[q * W0 + i] = z;
+      if (p0 + q < P) Z0[(size_t)i * P + p0 + q] = z;
+    }
+    __syncthreads();
+    for (int e = tid; e < W * TV; e += blockDim.x) {  // z1 (thread: feature i, point q; q fastest)
+      const int i = e / TV, q = e % TV;
+      double acc = v.b1[i];
+      for (int j = 0; j < W0; ++j) acc += v.W1[i * W0 + j] * sZ0[q * W0 + j];
+      const double z1 = tanh(acc);
+      sZ1[i * TV + q] = z1;
+      if (p0 + q < P) Z1[(size_t)i * P + p0 + q] = z1;
+    }
+    __syncthreads();
+    const int r0 = warp * 16;
+    {  // X = W2 z1 on the tensor cores
+      double acc[2][TV / 8][2] = {};
+      for (int k = 0; k < W; k += 4) {
+        const double a0 = __ldg(v.W2 + (r0 + lane / 4) * W + k + lane % 4);
+        const double a1 = __ldg(v.W2 + (r0 + 8 + lane / 4) * W + k + lane % 4);
+#pragma unroll
+        for (int j = 0; j < TV / 8; ++j) {
+          const double bv = sZ1[(k + lane % 4) * TV + 8 * j + lane / 4];
+          dmma(acc[0][j][0], acc[0][j][1], a0, bv);
+          dmma(acc[1][j][0], acc[1][j][1], a1, bv);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < TV / 8; ++j) {
+          const int r = r0 + 8 * i + lane / 4, q = 8 * j + 2 * (lane % 4);
+          sX[r * TV + q] = tanh(acc[i][j][0] + v.b2[r]);
+          sX[r * TV + q + 1] = tanh(acc[i][j][1] + v.b2[r]);
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < W * TV; e += blockDim.x) {
+      const int i = e / TV, q = e % TV;
+      if (p0 + q < P) Z2[(size_t)i * P + p0 + q] = sX[i * TV + q];
+    }
+    for (int e = tid; e < N * TV; e += blockDim.x) {  // o, d3 = w (1 - o^2)
+      const int i = e / TV, q = e % TV;
+      const size_t p = min(p0 + q, P - 1);
+      double acc = v.b3[i];
+      for (int l = 0; l < W; ++l) acc += v.W3[i * W + l] * sX[l * TV + q];
+      const double o = tanh(acc);
+      const int mm = 1 + (int)(p / nb), b = (int)(p % nb);
+      const double d3 = wq[(size_t)mm * row + (size_t)b * N + i] * (1.0 - o * o);
+      sD3[i * TV + q] = d3;
+      if (p0 + q < P) D3[(size_t)i * P + p0 + q] = d3;
+    }
+    __syncthreads();
+    for (int e = tid; e < W * TV; e += blockDim.x) {  // d2 = (W3^T d3)(1 - z2^2)
+      const int i = e / TV, q = e % TV;
+      double acc = 0.0;
+      for (int l = 0; l < N; ++l) acc += v.W3[l * W + i] * sD3[l * TV + q];
+      const double z2 = sX[i * TV + q];
+      const double d2 = acc * (1.0 - z2 * z2);
+      sD2[i * TV + q] = d2;
+      if (p0 + q < P) D2[(size_t)i * P + p0 + q] = d2;
+    }
+    __syncthreads();
+    {  // d1 = (W2^T d2)(1 - z1^2) on the tensor cores: A(i, k) = W2[k][i]
+      double acc[2][TV / 8][2] = {};
+      for (int k = 0; k < W; k += 4) {
+        const double a0 = __ldg(v.W2 + (k + lane % 4) * W + r0 + lane / 4);
+        const double a1 = __ldg(v.W2 + (k + lane % 4) * W + r0 + 8 + lane / 4);
+#pragma unroll
+        for (int j = 0; j < TV / 8; ++j) {
+          const double bv = sD2[(k + lane % 4) * TV + 8 * j + lane / 4];
+          dmma(acc[0][j][0], acc[0][j][1], a0, bv);
+          dmma(acc[1][j][0], acc[1][j][1], a1, bv);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < TV / 8; ++j) {
+          const int r = r0 + 8 * i + lane / 4, q = 8 * j + 2 * (lane % 4);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double z1 = sZ1[r * TV + q + h];
+            if (p0 + q + h < P) D1[(size_t)r * P + p0 + q + h] = acc[i][j][h] * (1.0 - z1 * z1);
+          }
+        }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace node
+
+cudaError_t launch_node_vectors_dmma(const DevModel& m, const double* states, const double* times, const double* wq,
+                                     int nb, size_t P, double* vec, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(node::node_vectors_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         node::kVecSmem);
+    attr = true;
+  }
+  node::node_vectors_dmma_kernel<<<2 * 148, node::kVecThreads, node::kVecSmem, st>>>(m, states, times, wq, nb, P,
+                                                                                      vec);
+  return cudaGetLastError();
+}
+
 bool node_fast_path(const DevModel& m) { return m.kind == 5 && m.n == node::N && m.W == node::W; }
 
 size_t node_scratch_doubles(int nb, int c) {

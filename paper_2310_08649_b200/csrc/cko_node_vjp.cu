@@ -125,7 +125,12 @@ cudaError_t launch_node_vjp(const DevModel& m, const double* states, const doubl
   const int n = m.n, W = m.W, w0 = n + 1;
   double* vec = scratch;
   double* partial = scratch + P * (size_t)(w0 + 4 * W + n);
-  node_vectors_kernel<<<4 * 148, 128, 0, st>>>(m, states, times, wq, nb, nt, vec, P);
+  if (node_fast_path(m)) {  // C4 shape: the two W x W products per point on the tensor cores (cko_node.cu)
+    cudaError_t e = launch_node_vectors_dmma(m, states, times, wq, nb, P, vec, st);
+    if (e != cudaSuccess) return e;
+  } else {
+    node_vectors_kernel<<<4 * 148, 128, 0, st>>>(m, states, times, wq, nb, nt, vec, P);
+  }
   const double* Z0 = vec;
   const double* Z1 = Z0 + (size_t)w0 * P;
   const double* Z2 = Z1 + (size_t)W * P;
