@@ -95,6 +95,60 @@ __global__ void __launch_bounds__(256) outer_partial_kernel(const double* A, int
     }
 }
 
+// DMMA form of outer_partial_kernel for R, C multiples of 8: a 64 x 64 output
+// tile per CTA (four warps of 32 x 32: 4 x 4 fragments of m8n8k4), K staged
+// through shared memory 32 points at a time, fixed K slices (deterministic).
+constexpr int kDT = 64, kDK = 32, kDKP = kDK + 4;
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(128) outer_partial_dmma_kernel(const double* A, int R, const double* B, int C,
+                                                                 size_t P, double* partial) {
+  __shared__ double sa[kDT][kDKP], sb[kDT][kDKP];
+  const int tilesC = (C + kDT - 1) / kDT;
+  const int i0 = (blockIdx.x / tilesC) * kDT, j0 = (blockIdx.x % tilesC) * kDT;
+  const int ks = blockIdx.y;
+  const size_t per = (P + gridDim.y - 1) / gridDim.y;
+  const size_t k0 = per * ks, k1 = min(P, k0 + per);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;  // warp's 32 x 32 block of the tile
+  double acc[4][4][2] = {};
+  for (size_t kc = k0; kc < k1; kc += kDK) {
+    for (int e = threadIdx.x; e < kDT * kDK; e += blockDim.x) {
+      const int r = e / kDK, q = e % kDK;
+      const size_t k = kc + q;
+      sa[r][q] = (i0 + r < R && k < k1) ? A[(size_t)(i0 + r) * P + k] : 0.0;
+      sb[r][q] = (j0 + r < C && k < k1) ? B[(size_t)(j0 + r) * P + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kDK; kk += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        av[f] = sa[wr + 8 * f + lane / 4][kk + lane % 4];
+        bv[f] = sb[wc + 8 * f + lane / 4][kk + lane % 4];
+      }
+#pragma unroll
+      for (int fr = 0; fr < 4; ++fr)
+#pragma unroll
+        for (int fc = 0; fc < 4; ++fc) dmma884(acc[fr][fc][0], acc[fr][fc][1], av[fr], bv[fc]);
+    }
+    __syncthreads();
+  }
+  double* out = partial + ((size_t)ks * R) * C;
+#pragma unroll
+  for (int fr = 0; fr < 4; ++fr)
+#pragma unroll
+    for (int fc = 0; fc < 4; ++fc) {
+      const int i = i0 + wr + 8 * fr + lane / 4, j = j0 + wc + 8 * fc + 2 * (lane % 4);
+      if (i < R && j < C) out[(size_t)i * C + j] = acc[fr][fc][0];
+      if (i < R && j + 1 < C) out[(size_t)i * C + j + 1] = acc[fr][fc][1];
+    }
+}
+
 __global__ void outer_reduce_kernel(const double* partial, int KS, int R, int C, double* out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < R * C; e += gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -105,6 +159,12 @@ __global__ void outer_reduce_kernel(const double* partial, int KS, int R, int C,
 
 cudaError_t outer_sum(const double* A, int R, const double* B, int C, size_t P, double* partial, double* out,
                       cudaStream_t st) {
+  if (B && R % 8 == 0 && C % 8 == 0) {  // tensor cores
+    const int tiles = ((R + kDT - 1) / kDT) * ((C + kDT - 1) / kDT);
+    outer_partial_dmma_kernel<<<dim3(tiles, kOuterKS), 128, 0, st>>>(A, R, B, C, P, partial);
+    outer_reduce_kernel<<<(R * C + 255) / 256, 256, 0, st>>>(partial, kOuterKS, R, C, out);
+    return cudaGetLastError();
+  }
   const int tiles = ((R + kTile - 1) / kTile) * ((C + kTile - 1) / kTile);
   outer_partial_kernel<<<dim3(tiles, kOuterKS), 256, 0, st>>>(A, R, B, C, P, partial);
   outer_reduce_kernel<<<(R * C + 255) / 256, 256, 0, st>>>(partial, kOuterKS, R, C, out);
