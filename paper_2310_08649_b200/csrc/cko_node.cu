@@ -52,7 +52,8 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // Points are (k, b) pairs of a chunk, p = k * nb + b, state rows at
 // states[(row0 + k) * nb * N + b * N], times t[(row0 + k) * nb + b]. H (P, N)
 // receives h, J (P, N, N) the Jacobian (when want_j).
-constexpr int kEvalSmem = (2 * W * BC + TP * W0 + TP * N) * 8;  // operand, products, z0, 1 - o^2
+// the products overwrite the operand once every warp has read it: ~75 KB, two CTAs per SM (registers)
+constexpr int kEvalSmem = (W * BC + TP * W0 + TP * N) * 8;  // operand / products, z0, 1 - o^2
 
 // Point p = k * nb + b sits on trajectory row row0 + dir * k (dir = -1: the
 // descending rows of a reversed adjoint chunk).
@@ -61,9 +62,9 @@ __global__ void __launch_bounds__(kEvalThreads) node_eval_kernel(DevModel m, con
                                                                  int P, double* H, double* J, int want_j) {
   extern __shared__ __align__(16) double smem[];
   double* sB = smem;               // operand  (W x 72) = 72 KB
-  double* sX = sB + W * BC;        // products (W x 72) = 72 KB
-  double (*sz0)[W0] = reinterpret_cast<double (*)[W0]>(sX + W * BC);
-  double (*sg3)[N] = reinterpret_cast<double (*)[N]>(sX + W * BC + TP * W0);
+  double* sX = sB;                 // products overwrite it after the tensor-core pass
+  double (*sz0)[W0] = reinterpret_cast<double (*)[W0]>(sB + W * BC);
+  double (*sg3)[N] = reinterpret_cast<double (*)[N]>(sB + W * BC + TP * W0);
   const Views v(m.p);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ntiles = (P + TP - 1) / TP;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(kEvalThreads) node_eval_kernel(DevModel m, con
           dmma(acc[1][j][0], acc[1][j][1], a1, bv);
         }
       }
+      __syncthreads();  // every warp is done with the operand
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -500,7 +502,7 @@ cudaError_t node_eval(const DevModel& m, const double* states, const double* tim
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, node::kEvalSmem);
   if (attr != cudaSuccess) return attr;
   const int tiles = (P + node::TP - 1) / node::TP;
-  node::node_eval_kernel<<<tiles < 148 ? tiles : 148, node::kEvalThreads, node::kEvalSmem, st>>>(
+  node::node_eval_kernel<<<tiles < 2 * 148 ? tiles : 2 * 148, node::kEvalThreads, node::kEvalSmem, st>>>(
       m, states, times, row0, dir, nb, P, H, J, want_j ? 1 : 0);
   return cudaGetLastError();
 }
