@@ -178,3 +178,18 @@ def test_mds_cross_lane_exchanges(port):
     got = api.gradient_adjoint(m, y0, api.TimeGrid(t), 6, ctx=ctx)
     assert ctx.kernel_generation_used() == 2
     _check(got, want)
+
+
+@pytest.mark.parametrize("nb,nt,nc", [(5000, 6, 3), (25000, 4, 4)])
+def test_mds_wide_ctas(port, nb, nt, nc):
+    """More lanes per CTA than one tile (nb = 5000: 2 lane tiles per CTA) and than the residual staging
+    holds at once (nb = 25000: ~169 lanes per CTA, staged in lane tiles)."""
+    m = P.build_mass_damper_spring(10, nb)
+    y0 = np.random.default_rng(nb).uniform(-1e-3, 1e-3, (nb, 20))
+    t = uniform_times(nt, nb, nt * 1e-6)
+    want = port.gradient(m, y0, t, nc)
+    assert want.loss > 0.0
+    ctx = _ctx(2)
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, ctx=ctx)
+    assert ctx.kernel_generation_used() == 2
+    _check(got, want)
