@@ -73,6 +73,32 @@ struct MdsS {
       h[NU + u] = acc;
     }
   }
+  // Rows of M = I - dt J (ndt = -dt) when the row kind is known: slot 0 is the
+  // position row u (J row = e_{NU+u}), slot 1 the velocity row NU + u — the
+  // v2 group layout with 10-lane groups holds exactly these. Same roundings
+  // as xadd(xmul(ndt, J_ij), [i == j]) on jac_row's entries.
+  static constexpr bool kSlotRows = true;
+  __device__ static void m_row_slot(const double* cs, int slot, int u, double ndt, double (&m)[N]) {
+    const double z = xmul(ndt, 0.0);
+    if (slot == 0) {
+#pragma unroll
+      for (int j = 0; j < NU; ++j) {
+        m[j] = j == u ? xadd(z, 1.0) : z;
+        m[NU + j] = j == u ? xmul(ndt, 1.0) : z;
+      }
+    } else {
+      const double am = u > 0 ? cs[u] : 0.0, cm = u > 0 ? cs[NU + u] : 0.0;
+      const double ap = u + 1 < NU ? cs[u + 1] : 0.0, cp = u + 1 < NU ? cs[NU + u + 1] : 0.0;
+      const double a0 = (0.0 + am) + ap, c0 = (0.0 + cm) + cp;
+      const double ka = xmul(ndt, a0), km = xmul(ndt, -am), kp = xmul(ndt, -ap);
+      const double ca = xadd(xmul(ndt, c0), 1.0), cmv = xmul(ndt, -cm), cpv = xmul(ndt, -cp);
+#pragma unroll
+      for (int j = 0; j < NU; ++j) {
+        m[j] = j == u ? ka : (j + 1 == u ? km : (j == u + 1 ? kp : z));
+        m[NU + j] = j == u ? ca : (j + 1 == u ? cmv : (j == u + 1 ? cpv : z));
+      }
+    }
+  }
   // Row i of the analytic Jacobian (models_mds.cpp:54-82); the state does not
   // enter. Written as per-entry selects so the row stays in registers.
   __device__ static void jac_row(const DevModel&, const double* cs, double, const double (&)[N], int i,

@@ -86,6 +86,10 @@ constexpr bool kLookahead = CKO_LOOKAHEAD;  // group LU publishes row c + 1 duri
 #define CKO_FWD_SHARED_JAC 0
 #endif
 constexpr bool kFwdSharedJac = CKO_FWD_SHARED_JAC;
+#ifndef CKO_FWD_SLOT_ROWS
+#define CKO_FWD_SLOT_ROWS 0
+#endif
+constexpr bool kFwdSlotRows = CKO_FWD_SLOT_ROWS;  // MDS rows by kind (no per-entry kind selects)
 #ifndef CKO_FWD_PRED
 #define CKO_FWD_PRED 0
 #endif
@@ -118,6 +122,16 @@ struct HasConstJac {
 template <class MS>
 struct HasConstJac<MS, std::void_t<decltype(MS::kConstJac)>> {
   static constexpr bool value = MS::kConstJac;
+};
+
+// Models that build M row by row kind in the 10-lane group layout (MdsS).
+template <class MS, class = void>
+struct HasSlotRows {
+  static constexpr bool value = false;
+};
+template <class MS>
+struct HasSlotRows<MS, std::void_t<decltype(MS::kSlotRows)>> {
+  static constexpr bool value = MS::kSlotRows;
 };
 
 // Per-group pivot-row buffer: two rows of N + 2 doubles (16-byte aligned halves).
@@ -801,7 +815,9 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         for (int q = 0; q < Gm::R; ++q) {
           const int i = gl + q * Gm::G;
           if (i < N) {
-            if constexpr (kFwdSharedJac && HasConstJac<MS>::value) {  // M = -dt J + I from shared memory
+            if constexpr (kFwdSlotRows && HasSlotRows<MS>::value && Gm::G == MS::N / 2) {
+              MS::m_row_slot(cs, q, gl, ndt, m[q]);  // lane gl: position row gl, velocity row N/2 + gl
+            } else if constexpr (kFwdSharedJac && HasConstJac<MS>::value) {  // M = -dt J + I from shared memory
               const double* Jr = cs + MS::JOFF + i * N;
               const double* Er = MS::unit_row(cs, i);
 #pragma unroll
