@@ -262,6 +262,58 @@ def c3_pcr_vs_sequential(ctx, reps=2):
     return out
 
 
+def c2_solver_family(args, local, nt_s=500, reps=2):
+    """The headline workload's chunked solver family on this GPU, bounded sample (nb lanes x nt_s steps,
+    same dt), device-resident through the C ABI and timed with the kernels' own CUDA events: Thomas (the
+    bench line's solver) next to PCR and hybrid at their best measured chunk, so the metric's PCR member is
+    on record (~40x the fp64 work of Thomas at n = 20)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2310_08649_b200 as P
+    from paper_2310_08649_b200 import abi, api
+    from paper_2310_08649_b200._native import lib
+    from paper_2310_08649_b200.errors import raise_for
+    L = lib()
+    ctx = api.Context(local)
+    m = P.build_mass_damper_spring(args.n_unit, args.nb)
+    nb, n = args.nb, m.state_size
+    dm = ctx.model(m)
+    d_times = torch.from_numpy(uniform_times(nt_s, nb, args.t_max * nt_s / args.nt)).cuda()
+    d_y0 = torch.zeros((nb, n), dtype=torch.float64, device="cuda")
+    d_states = torch.empty((nt_s + 1, nb * n), dtype=torch.float64, device="cuda")
+    grad = np.zeros(m.params.size)
+    loss = C.c_double()
+    st = api.NewtonSettings().c()
+    wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+    kms = (C.c_double * 4)()
+    L.cko_ctx_enable_timing(ctx.h, 1)
+    out = {}
+    for name, kind, nc in (("thomas", 0, args.n_chunk), ("pcr", 1, 4), ("hybrid", 2, 16)):
+        sv = api.SolverChoice(kind, 1).c()
+        tot = 0.0
+        for it in range(reps + 1):
+            raise_for(L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()),
+                                              nb, nt_s, nc, C.byref(st), C.byref(sv),
+                                              C.c_void_p(d_states.data_ptr()), C.byref(wf), C.byref(e)), e)
+            L.cko_ctx_last_kernel_ms(ctx.h, kms)
+            f_ms = kms[0]
+            raise_for(L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()),
+                                              C.c_void_p(d_times.data_ptr()), nb, nt_s, nc, C.byref(sv),
+                                              abi.CKO_LOSS_FROBENIUS, None, C.byref(loss), abi.dptr(grad),
+                                              C.byref(wb), C.byref(e)), e)
+            L.cko_ctx_last_kernel_ms(ctx.h, kms)
+            if it:  # the first pass warms up
+                tot += f_ms + kms[1] + kms[2] + kms[3]
+        ms = tot / reps
+        out[name] = {"n_chunk": nc, "series_steps_per_s": nb * nt_s / (ms * 1e-3), "kernel_ms": ms,
+                     "kernel_generation": ctx.kernel_generation_used()}
+    L.cko_ctx_enable_timing(ctx.h, 0)
+    out["sample"] = f"nb={nb} x nt={nt_s} (dt as the full grid), device-resident, kernel time"
+    return out
+
+
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
@@ -427,6 +479,10 @@ def main():
         line["roofline"]["traffic"] = traffic["bytes_per_launch"]
         line["roofline"]["traffic_source"] = traffic["source"]
     if world == 1 and not args.no_c3:
+        try:
+            line["c2_solver_family"] = c2_solver_family(args, local)
+        except Exception as ex:  # side measurement only
+            line["c2_solver_family"] = {"error": str(ex)[:200]}
         try:
             line["c3_pcr_vs_sequential"] = c3_pcr_vs_sequential(api.Context(local))
         except Exception as ex:
