@@ -34,7 +34,7 @@ namespace v2 {
 template <int N>
 struct Geo {
 #ifndef CKO_G20
-#define CKO_G20 10
+#define CKO_G20 10  // lanes per group for 17 <= n <= 20 (knob; 7 spills)
 #endif
   static constexpr int G = N <= 8 ? 1 : (N <= 16 ? 8 : (N <= 20 ? CKO_G20 : 16));
   static constexpr int R = (N + G - 1) / G;
@@ -66,34 +66,36 @@ constexpr int kMaxSlots = 7;  // record slots: named barriers 1..2Q must stay be
 constexpr int kSmemCap = 224 * 1024;
 constexpr int kRoundBarrier = 15;  // producers only; ring barriers use 1 .. 2Q <= 14
 constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruction-cache locality)
+
+// Tuning knobs: compile-time, A/B-tested with scripts/build_variant.sh and
+// scripts/gpu_variants.sh / gpu_cmp_dt.sh; the defaults are the measured best
+// (DESIGN.md section 7 lists what each alternative cost).
 #ifndef CKO_ROUND_PER_SMSP
-#define CKO_ROUND_PER_SMSP 1
-#endif
-#ifndef CKO_XCHG2
-#define CKO_XCHG2 2  // 0: all-rows swap through the record; 1: shuffle argmax + 2-lane swap; 2: scan + 2-lane swap
+#define CKO_ROUND_PER_SMSP 1  // round barrier among the 3 producer warps of each SMSP (0: all 9)
 #endif
 #ifndef CKO_ROUND_EVERY
-#define CKO_ROUND_EVERY 1
+#define CKO_ROUND_EVERY 1  // rounds between producer barriers
 #endif
-constexpr int kRoundEvery = CKO_ROUND_EVERY;  // rounds between producer barriers
+#ifndef CKO_XCHG2
+#define CKO_XCHG2 2  // row exchange: 0 all rows through the record; 1 shuffle argmax + owner lanes; 2 scan + owner lanes
+#endif
 #ifndef CKO_LOOKAHEAD
-#define CKO_LOOKAHEAD 0
+#define CKO_LOOKAHEAD 0  // group LU publishes row c + 1 during column c
 #endif
-constexpr bool kLookahead = CKO_LOOKAHEAD;  // group LU publishes row c + 1 during column c
-// The forward builds M from the model's per-entry selects (ALU) rather than
-// the shared-memory J rows: its LU already loads the shared-memory pipe.
 #ifndef CKO_FWD_SHARED_JAC
-#define CKO_FWD_SHARED_JAC 0
+#define CKO_FWD_SHARED_JAC 0  // forward builds M from the shared-memory J rows instead of per-entry selects
 #endif
-constexpr bool kFwdSharedJac = CKO_FWD_SHARED_JAC;
 #ifndef CKO_FWD_SLOT_ROWS
-#define CKO_FWD_SLOT_ROWS 0
+#define CKO_FWD_SLOT_ROWS 0  // forward builds MDS rows by kind (position / velocity slot)
 #endif
-constexpr bool kFwdSlotRows = CKO_FWD_SLOT_ROWS;  // MDS rows by kind (no per-entry kind selects)
 #ifndef CKO_FWD_PRED
-#define CKO_FWD_PRED 0
+#define CKO_FWD_PRED 0  // predicated (not branched) trailing update in the forward LU
 #endif
-constexpr bool kFwdPred = CKO_FWD_PRED;  // predicated trailing update in the forward LU
+constexpr int kRoundEvery = CKO_ROUND_EVERY;
+constexpr bool kLookahead = CKO_LOOKAHEAD;
+constexpr bool kFwdSharedJac = CKO_FWD_SHARED_JAC;
+constexpr bool kFwdSlotRows = CKO_FWD_SLOT_ROWS;
+constexpr bool kFwdPred = CKO_FWD_PRED;
 constexpr int kMaxWs = 3;     // producer warps per slot
 
 // Shared-memory record of one factored point (doubles): the LU factors in
@@ -533,7 +535,7 @@ __device__ inline bool factor_block(const Build& build, const Rows& rows, int gl
 template <int N>
 __device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* vs, double (&v)[N]) {
 #ifndef CKO_SOLVE_B
-#define CKO_SOLVE_B 4
+#define CKO_SOLVE_B 4  // substitution rows per block (knob; 2 / 5 / 8 measured equal or slower)
 #endif
   constexpr int B = CKO_SOLVE_B;
   const double* rec = static_cast<const double*>(__builtin_assume_aligned(rec_in, 16));
