@@ -253,18 +253,52 @@ __device__ inline void rec_solve(const double* rec, double (&v)[N]) {
   for (int i = 0; i < N; ++i) v[i] = y[i];
 }
 
+// The substitution kernels run one thread per lane (a few warps on the whole
+// GPU): each thread streams its rows' records and right-hand sides into its
+// own shared-memory ring with cp.async, kSubD rows ahead of the solve, so the
+// L2 latency leaves the dependency chain.
+constexpr int kSubD = 4;                 // rows in flight per thread
+constexpr int kSubS = kRec + N;          // staged doubles per row: record | rhs (16-byte multiple)
+constexpr int kSubThreads = 64;
+constexpr int kSubSmem = kSubThreads * kSubD * kSubS * 8;
+static_assert(kRec % 2 == 0 && kSubS % 2 == 0, "16-byte staging");
+
+__device__ __forceinline__ void sub_stage(double* dst, const double* rec, const double* rhs) {
+  for (int e = 0; e < kRec; e += 2) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst + e);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(rec + e) : "memory");
+  }
+  for (int e = 0; e < N; e += 2) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst + kRec + e);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(rhs + e) : "memory");
+  }
+}
+__device__ __forceinline__ void sub_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void sub_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(kSubD - 1) : "memory"); }
+
 // Thread per lane: forward substitution x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k.
-__global__ void node_thomas_fwd_kernel(double* states, const double* R, const double* recs, int step, int c,
-                                       int nb) {
+__global__ void __launch_bounds__(kSubThreads) node_thomas_fwd_kernel(double* states, const double* R,
+                                                                      const double* recs, int step, int c, int nb) {
+  extern __shared__ __align__(16) double sub_smem[];
+  double* my = sub_smem + (size_t)threadIdx.x * kSubD * kSubS;
   const size_t row = (size_t)nb * N;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    for (int k = 0; k < kSubD - 1; ++k) {
+      if (k < c) sub_stage(my + k * kSubS, recs + ((size_t)k * nb + b) * kRec, R + ((size_t)k * nb + b) * N);
+      sub_commit();
+    }
     double x[N];
     for (int i = 0; i < N; ++i) x[i] = 0.0;
     for (int k = 0; k < c; ++k) {
-      const int p = k * nb + b;
+      const int kn = k + kSubD - 1;
+      if (kn < c)
+        sub_stage(my + (kn % kSubD) * kSubS, recs + ((size_t)kn * nb + b) * kRec, R + ((size_t)kn * nb + b) * N);
+      sub_commit();
+      sub_wait();
+      const double* st = my + (k % kSubD) * kSubS;
       double v[N];
-      for (int i = 0; i < N; ++i) v[i] = R[(size_t)p * N + i] + x[i];
-      rec_solve(recs + (size_t)p * kRec, v);
+      for (int i = 0; i < N; ++i) v[i] = st[kRec + i] + x[i];
+      rec_solve(st, v);
       double* yy = states + (size_t)(step + 1 + k) * row + (size_t)b * N;
       for (int i = 0; i < N; ++i) {
         x[i] = v[i];
@@ -297,17 +331,30 @@ __global__ void node_adj_rhs_kernel(const double* states, const double* times, c
 }
 
 // Thread per lane: delta_r = M_r^{-1}(rhs_r + delta_{r-1}), w_m = (lambda + delta_r) dt, lambda += delta_{c-1}.
-__global__ void node_thomas_adj_kernel(const double* R, const double* recs, const double* times, int step_hi,
-                                       int c, int nb, double* lam, double* wq) {
+__global__ void __launch_bounds__(kSubThreads) node_thomas_adj_kernel(const double* R, const double* recs,
+                                                                      const double* times, int step_hi, int c,
+                                                                      int nb, double* lam, double* wq) {
+  extern __shared__ __align__(16) double sub_smem[];
+  double* my = sub_smem + (size_t)threadIdx.x * kSubD * kSubS;
   const size_t row = (size_t)nb * N;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    for (int r = 0; r < kSubD - 1; ++r) {
+      if (r < c) sub_stage(my + r * kSubS, recs + ((size_t)r * nb + b) * kRec, R + ((size_t)r * nb + b) * N);
+      sub_commit();
+    }
     double d[N], lc[N];
     for (int i = 0; i < N; ++i) d[i] = 0.0, lc[i] = lam[(size_t)b * N + i];
     for (int r = 0; r < c; ++r) {
-      const int p = r * nb + b, m = step_hi - r;
+      const int m = step_hi - r;
+      const int rn = r + kSubD - 1;
+      if (rn < c)
+        sub_stage(my + (rn % kSubD) * kSubS, recs + ((size_t)rn * nb + b) * kRec, R + ((size_t)rn * nb + b) * N);
+      sub_commit();
+      sub_wait();
+      const double* st = my + (r % kSubD) * kSubS;
       const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
-      for (int i = 0; i < N; ++i) d[i] = R[(size_t)p * N + i] + d[i];
-      rec_solve(recs + (size_t)p * kRec, d);
+      for (int i = 0; i < N; ++i) d[i] = st[kRec + i] + d[i];
+      rec_solve(st, d);
       double* w = wq + (size_t)m * row + (size_t)b * N;
       for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
     }
@@ -548,7 +595,10 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
       ++it;
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
       node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step, c, nb, 0, recs, sing_key, 0, nc);
-      node_thomas_fwd_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(states, R, recs, step, c, nb);
+      static const cudaError_t fattr = cudaFuncSetAttribute(
+          (const void*)node_thomas_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubSmem);
+      if (fattr != cudaSuccess) return fattr;
+      node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(states, R, recs, step, c, nb);
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
       node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, 0, tol_a,
@@ -594,7 +644,11 @@ cudaError_t node_adjoint(const DevModel& m, const double* states, const double* 
     if ((e = node_eval(m, states, times, step_hi, -1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
     node_adj_rhs_kernel<<<blocks_for(P, 128), 128, 0, st>>>(states, times, Jb, dL, loss, lam, step_hi, c, nb, R);
     node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step_hi, c, nb, 1, recs, sing_key, ord, nc);
-    node_thomas_adj_kernel<<<blocks_for(nb, 64), 64, 0, st>>>(R, recs, times, step_hi, c, nb, lam, wq);
+    static const cudaError_t aattr = cudaFuncSetAttribute(
+        (const void*)node_thomas_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubSmem);
+    if (aattr != cudaSuccess) return aattr;
+    node_thomas_adj_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(R, recs, times, step_hi, c,
+                                                                                        nb, lam, wq);
     step_hi -= c;
     ++ord;
   }
