@@ -98,29 +98,57 @@ __global__ void __launch_bounds__(256) outer_partial_kernel(const double* A, int
 // DMMA form of outer_partial_kernel for R, C multiples of 8: a 64 x 64 output
 // tile per CTA (four warps of 32 x 32: 4 x 4 fragments of m8n8k4), K staged
 // through shared memory 32 points at a time, fixed K slices (deterministic).
-constexpr int kDT = 64, kDK = 32, kDKP = kDK + 4;
+constexpr int kDT = 64, kDK = 16, kDKP = kDK + 4;
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void stage_tile(double (*sa)[kDKP], double (*sb)[kDKP], const double* A, int R,
+                                           const double* B, int C, size_t P, int i0, int j0, size_t kc, size_t k1) {
+  // 16-byte cp.async where the whole pair is inside the slice, zero-fill otherwise (rows of A / B are P long)
+  for (int e = threadIdx.x; e < kDT * (kDK / 2); e += blockDim.x) {
+    const int r = e / (kDK / 2), q = 2 * (e % (kDK / 2));
+    const size_t k = kc + q;
+    const bool full = k + 1 < k1 && (P % 2 == 0);
+    if (i0 + r < R && full) {
+      const unsigned s = (unsigned)__cvta_generic_to_shared(&sa[r][q]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(A + (size_t)(i0 + r) * P + k) : "memory");
+    } else {
+      sa[r][q] = (i0 + r < R && k < k1) ? A[(size_t)(i0 + r) * P + k] : 0.0;
+      sa[r][q + 1] = (i0 + r < R && k + 1 < k1) ? A[(size_t)(i0 + r) * P + k + 1] : 0.0;
+    }
+    if (j0 + r < C && full) {
+      const unsigned s = (unsigned)__cvta_generic_to_shared(&sb[r][q]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(B + (size_t)(j0 + r) * P + k) : "memory");
+    } else {
+      sb[r][q] = (j0 + r < C && k < k1) ? B[(size_t)(j0 + r) * P + k] : 0.0;
+      sb[r][q + 1] = (j0 + r < C && k + 1 < k1) ? B[(size_t)(j0 + r) * P + k + 1] : 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(128) outer_partial_dmma_kernel(const double* A, int R, const double* B, int C,
                                                                  size_t P, double* partial) {
-  __shared__ double sa[kDT][kDKP], sb[kDT][kDKP];
+  __shared__ __align__(16) double sa[2][kDT][kDKP], sb[2][kDT][kDKP];  // double-buffered K stages
   const int tilesC = (C + kDT - 1) / kDT;
   const int i0 = (blockIdx.x / tilesC) * kDT, j0 = (blockIdx.x % tilesC) * kDT;
   const int ks = blockIdx.y;
-  const size_t per = (P + gridDim.y - 1) / gridDim.y;
-  const size_t k0 = per * ks, k1 = min(P, k0 + per);
+  size_t per = (P + gridDim.y - 1) / gridDim.y;
+  per = (per + 1) & ~(size_t)1;  // even slice starts keep the 16-byte copies aligned
+  const size_t k0 = min(P, per * ks), k1 = min(P, k0 + per);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wr = (warp >> 1) * 32, wc = (warp & 1) * 32;  // warp's 32 x 32 block of the tile
   double acc[4][4][2] = {};
-  for (size_t kc = k0; kc < k1; kc += kDK) {
-    for (int e = threadIdx.x; e < kDT * kDK; e += blockDim.x) {
-      const int r = e / kDK, q = e % kDK;
-      const size_t k = kc + q;
-      sa[r][q] = (i0 + r < R && k < k1) ? A[(size_t)(i0 + r) * P + k] : 0.0;
-      sb[r][q] = (j0 + r < C && k < k1) ? B[(size_t)(j0 + r) * P + k] : 0.0;
+  int buf = 0;
+  if (k0 < k1) stage_tile(sa[0], sb[0], A, R, B, C, P, i0, j0, k0, k1);
+  for (size_t kc = k0; kc < k1; kc += kDK, buf ^= 1) {
+    if (kc + kDK < k1) {
+      stage_tile(sa[buf ^ 1], sb[buf ^ 1], A, R, B, C, P, i0, j0, kc + kDK, k1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
 #pragma unroll
@@ -128,8 +156,8 @@ __global__ void __launch_bounds__(128) outer_partial_dmma_kernel(const double* A
       double av[4], bv[4];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
-        av[f] = sa[wr + 8 * f + lane / 4][kk + lane % 4];
-        bv[f] = sb[wc + 8 * f + lane / 4][kk + lane % 4];
+        av[f] = sa[buf][wr + 8 * f + lane / 4][kk + lane % 4];
+        bv[f] = sb[buf][wc + 8 * f + lane / 4][kk + lane % 4];
       }
 #pragma unroll
       for (int fr = 0; fr < 4; ++fr)
