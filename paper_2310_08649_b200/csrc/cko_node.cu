@@ -188,6 +188,52 @@ __global__ void node_residual_kernel(const double* states, const double* times, 
   }
 }
 
+// Point-parallel form for chunks of at most 128 rows: a block holds 128 / c
+// lanes x c rows, one thread per point, then one thread per lane sums the
+// rows' squared norms in order (same arithmetic as node_residual_kernel).
+__global__ void __launch_bounds__(128) node_residual_pp_kernel(const double* states, const double* times,
+                                                               const double* H, int step, int c, int nb, double* R,
+                                                               double* r0, double* rn, int first, double tol_a,
+                                                               double tol_r, unsigned* flags) {
+  __shared__ double ps[128];
+  const size_t row = (size_t)nb * N;
+  const int Lb = 128 / c, b0 = blockIdx.x * Lb;
+  const int k = threadIdx.x / Lb, lb = threadIdx.x % Lb, b = b0 + lb;
+  if (k < c && b < nb) {
+    const int p = k * nb + b;
+    const double t = times[(size_t)(step + 1 + k) * nb + b];
+    const double dt = t - times[(size_t)(step + k) * nb + b];
+    const double* y = states + (size_t)(step + 1 + k) * row + (size_t)b * N;
+    const double* ym = states + (size_t)(step + k) * row + (size_t)b * N;
+    double yv[N], ymv[N], hv[N];
+    for (int i = 0; i < N; ++i) yv[i] = y[i], ymv[i] = ym[i], hv[i] = H[(size_t)p * N + i];
+    double sq = 0.0;
+    for (int i = 0; i < N; ++i) {
+      const double vv = xsub(xsub(yv[i], ymv[i]), xmul(hv[i], dt));
+      R[(size_t)p * N + i] = vv;
+      sq = xadd(sq, xmul(vv, vv));
+    }
+    ps[k * Lb + lb] = sq;
+  }
+  __syncthreads();
+  if (threadIdx.x < Lb && b0 + (int)threadIdx.x < nb) {
+    const int bl = b0 + threadIdx.x;
+    double acc = 0.0;
+    for (int kk = 0; kk < c; ++kk) acc = xadd(acc, ps[kk * Lb + threadIdx.x]);
+    const double nrm = sqrt(acc);
+    double base = nrm;
+    if (first)
+      r0[bl] = nrm;
+    else
+      base = r0[bl];
+    rn[bl] = nrm;
+    unsigned f = 0;
+    if (!isfinite(nrm)) f |= FLAG_NON_FINITE;
+    if (!(nrm <= tol_a || nrm <= xmul(tol_r, base))) f |= FLAG_NOT_CONVERGED;
+    if (f) atomicOr(flags, f);
+  }
+}
+
 constexpr int kRec = N * N + N + 6;  // LU | 1/U_ii | perm (N + 1 ints) — 16-byte aligned stride
 
 // Thread per point: assemble M (forward: I - J dt; adjoint: (I - J dt)^T and the rhs
@@ -554,6 +600,20 @@ cudaError_t node_eval(const DevModel& m, const double* states, const double* tim
   return cudaGetLastError();
 }
 
+static void launch_node_residual(const double* states, const double* times, const double* H, int step, int c, int nb,
+                                 double* R, double* r0, double* rn, int first, double tol_a, double tol_r,
+                                 unsigned* flags, cudaStream_t st) {
+  using namespace node;
+  if (c <= 128) {
+    const int Lb = 128 / c;
+    node_residual_pp_kernel<<<(nb + Lb - 1) / Lb, 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, first,
+                                                                tol_a, tol_r, flags);
+  } else {
+    node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, first, tol_a,
+                                                             tol_r, flags);
+  }
+}
+
 // Host-driven Newton integration for the wide neural ODE (Thomas solver).
 // Returns 0 ok, 1 singular (key), 2 divergence (info), 4 group timeout.
 cudaError_t node_forward(const DevModel& m, double* states, const double* times, const double* dy, int nb, int nt,
@@ -583,8 +643,7 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
     node_init_chunk_kernel<<<blocks_for((size_t)P * N, 256), 256, 0, st>>>(states, dy, step, c, nb);
     if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
-    node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, 1, tol_a,
-                                                               tol_r, d_flags);
+    launch_node_residual(states, times, H, step, c, nb, R, r0, rn, 1, tol_a, tol_r, d_flags, st);
     unsigned f = 0;
     if ((e = flags(f)) != cudaSuccess) return e;
     int it = 0;
@@ -601,8 +660,7 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
       node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(states, R, recs, step, c, nb);
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
-      node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, 0, tol_a,
-                                                                 tol_r, d_flags);
+      launch_node_residual(states, times, H, step, c, nb, R, r0, rn, 0, tol_a, tol_r, d_flags, st);
       if ((e = flags(f)) != cudaSuccess) return e;
       unsigned long long key = ~0ull;
       if ((e = cudaMemcpyAsync(h_flags + 2, sing_key, sizeof key, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
