@@ -319,6 +319,38 @@ __device__ __forceinline__ void sub_stage(double* dst, const double* rec, const 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(rhs + e) : "memory");
   }
 }
+// rec_solve on a staged record: the permuted gather goes through the staged
+// rhs slot (already consumed) instead of a dynamically indexed register array.
+__device__ inline void rec_solve_staged(double* st, double (&v)[N]) {
+  const int* perm = reinterpret_cast<const int*>(st + N * N + N);
+  double y[N];
+  if (perm[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i] = v[i];
+  } else {
+    double* sc = st + kRec;
+#pragma unroll
+    for (int i = 0; i < N; ++i) sc[i] = v[i];
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i] = sc[perm[i]];
+  }
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    double s = y[i];
+#pragma unroll
+    for (int j = 0; j < i; ++j) s -= st[i * N + j] * y[j];
+    y[i] = s;
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    double s = y[i];
+#pragma unroll
+    for (int j = i + 1; j < N; ++j) s -= st[i * N + j] * y[j];
+    y[i] = s * st[N * N + i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = y[i];
+}
 __device__ __forceinline__ void sub_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void sub_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(kSubD - 1) : "memory"); }
 
@@ -341,10 +373,10 @@ __global__ void __launch_bounds__(kSubThreads) node_thomas_fwd_kernel(double* st
         sub_stage(my + (kn % kSubD) * kSubS, recs + ((size_t)kn * nb + b) * kRec, R + ((size_t)kn * nb + b) * N);
       sub_commit();
       sub_wait();
-      const double* st = my + (k % kSubD) * kSubS;
+      double* st = my + (k % kSubD) * kSubS;
       double v[N];
       for (int i = 0; i < N; ++i) v[i] = st[kRec + i] + x[i];
-      rec_solve(st, v);
+      rec_solve_staged(st, v);
       double* yy = states + (size_t)(step + 1 + k) * row + (size_t)b * N;
       for (int i = 0; i < N; ++i) {
         x[i] = v[i];
@@ -397,10 +429,10 @@ __global__ void __launch_bounds__(kSubThreads) node_thomas_adj_kernel(const doub
         sub_stage(my + (rn % kSubD) * kSubS, recs + ((size_t)rn * nb + b) * kRec, R + ((size_t)rn * nb + b) * N);
       sub_commit();
       sub_wait();
-      const double* st = my + (r % kSubD) * kSubS;
+      double* st = my + (r % kSubD) * kSubS;
       const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
       for (int i = 0; i < N; ++i) d[i] = st[kRec + i] + d[i];
-      rec_solve(st, d);
+      rec_solve_staged(st, d);
       double* w = wq + (size_t)m * row + (size_t)b * N;
       for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
     }
