@@ -247,31 +247,41 @@ __global__ void node_factor_kernel(const double* J, const double* times, int ste
     const double dt = times[(size_t)m * nb + b] - times[(size_t)(m - 1) * nb + b];
     const double* Jp = J + (size_t)p * N * N;
     double* rec = recs + (size_t)p * kRec;
+    // factor in a thread-local copy (L1-resident local memory), then store the record once
+    __align__(16) double loc[N * N + N];
     double mx = 0.0;
     auto build = [&]() {
+      double jv[N * N];
+#pragma unroll
+      for (int e = 0; e < N * N; ++e) jv[e] = Jp[e];  // every load in flight at once
+#pragma unroll
       for (int i = 0; i < N; ++i)
+#pragma unroll
         for (int j = 0; j < N; ++j) {
           double vv;
           if (adjoint)
-            vv = (i == j) ? 1.0 - dt * Jp[j * N + i] : -dt * Jp[j * N + i];
+            vv = (i == j) ? 1.0 - dt * jv[j * N + i] : -dt * jv[j * N + i];
           else
-            vv = (i == j) ? xadd(xmul(-dt, Jp[i * N + j]), 1.0) : xmul(-dt, Jp[i * N + j]);
-          rec[i * N + j] = vv;
+            vv = (i == j) ? xadd(xmul(-dt, jv[i * N + j]), 1.0) : xmul(-dt, jv[i * N + j]);
+          loc[i * N + j] = vv;
           mx = fmax(mx, fabs(vv));
         }
     };
     build();
     bool viol;
-    bool ok = lt::lu_thread_nopiv<N>(rec, rec + N * N, 1e-14 * mx, viol);
+    bool ok = lt::lu_thread_nopiv<N>(loc, loc + N * N, 1e-14 * mx, viol);
     int* perm = reinterpret_cast<int*>(rec + N * N + N);
     if (viol) {
       build();
-      ok = lt::lu_thread_pivot<N>(rec, rec + N * N, perm, 1e-14 * mx);
+      ok = lt::lu_thread_pivot<N>(loc, loc + N * N, perm, 1e-14 * mx);
       perm[N] = 0;
     } else {
       for (int i = 0; i < N; ++i) perm[i] = i;
       perm[N] = 1;
     }
+#pragma unroll
+    for (int e = 0; e < N * N + N; e += 2)
+      *reinterpret_cast<double2*>(rec + e) = make_double2(loc[e], loc[e + 1]);
     if (!ok)
       atomicMin(sing_key, adjoint ? ord * (unsigned long long)nc * nb + (unsigned long long)k * nb + b
                                   : (unsigned long long)k * nb + b);
