@@ -42,7 +42,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--nb", type=int, default=1000, help="series per GPU")
+    ap.add_argument("--nb", type=int, default=1000, help="series per GPU (--scaling weak)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: nb series per GPU; strong: --nb-total series split over the GPUs (north-star target)")
+    ap.add_argument("--nb-total", type=int, default=1000, help="series over all GPUs (--scaling strong)")
     ap.add_argument("--nt", type=int, default=10000)
     ap.add_argument("--n-unit", type=int, default=10)
     ap.add_argument("--t-max", type=float, default=0.01)
@@ -51,7 +54,7 @@ def parse():
     ap.add_argument("--n-switch", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-steps", type=int, default=32)
+    ap.add_argument("--cpu-sample-steps", type=int, default=0, help="CPU sample steps (0: one chunk, n_chunk)")
     ap.add_argument("--quiet-clocks", action="store_true", help="skip nvidia-smi sampling (profiler runs)")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 chunked-PCR vs sequential side measurement")
     return ap.parse_args()
@@ -158,23 +161,60 @@ def dist_env():
     return rank, world, local
 
 
+def lane_split(args, world, rank):
+    """(lanes of this rank, global lane offset, lanes over all ranks): weak scaling gives every rank
+    args.nb lanes; strong scaling splits args.nb_total contiguously (the first nb_total % world ranks get
+    one more lane)."""
+    if args.scaling == "weak":
+        return args.nb, rank * args.nb, args.nb * world
+    base, extra = divmod(args.nb_total, world)
+    nb = base + (1 if rank < extra else 0)
+    off = rank * base + min(rank, extra)
+    return nb, off, args.nb_total
+
+
 def mds_workload(args, world, rank):
     import paper_2310_08649_b200 as P
-    nb_total = args.nb * world
+    nb, off, nb_total = lane_split(args, world, rank)
     model = P.build_mass_damper_spring(args.n_unit, nb_total)
-    times = uniform_times(args.nt, args.nb, args.t_max)
-    y0 = np.zeros((args.nb, model.state_size))
-    return model.shard(rank * args.nb), y0, times
+    times = uniform_times(args.nt, nb, args.t_max)
+    y0 = np.zeros((nb, model.state_size))
+    return model.shard(off), y0, times
+
+
+def golden_parity(args, nb_total, loss, grad, wf, wb):
+    """The bench run's loss / gradient / WorkCounters against the compiled reference's own full-size run
+    (tests/golden/full_c2.npz, oracle/make_golden_full.py) when the workload is that configuration."""
+    path = os.path.join(ROOT, "tests", "golden", "full_c2.npz")
+    if not os.path.exists(path):
+        return {"checked": False, "why": "tests/golden/full_c2.npz missing"}
+    g = np.load(path)
+    same = (nb_total == int(g["nb"]) and args.nt == int(g["nt"]) and args.n_chunk == int(g["n_chunk"])
+            and args.solver == "thomas" and args.n_unit == int(g["n_unit"]) and args.t_max == float(g["t_max"]))
+    if not same:
+        return {"checked": False, "why": "workload differs from the golden's (C2, nb=1000, nt=10000, thomas/100)"}
+    keys = [k for k, _ in __import__("paper_2310_08649_b200.abi", fromlist=["x"]).CkoWork._fields_]
+    gl = float(g["thomas_loss"])
+    loss_rel = abs(loss - gl) / abs(gl)
+    grad_rel = float(np.max(np.abs(grad - g["thomas_grad"])) / np.max(np.abs(g["thomas_grad"])))
+    cnt = ([int(getattr(wf, k)) for k in keys] == [int(x) for x in g["thomas_fwd"]]
+           and [int(getattr(wb, k)) for k in keys] == [int(x) for x in g["thomas_bwd"]])
+    return {"checked": True, "against": "compiled reference, full C2 (tests/golden/full_c2.npz)",
+            "loss_rel": loss_rel, "grad_rel_max": grad_rel, "counters_equal": cnt,
+            "ok": bool(cnt and loss_rel <= 1e-10 and grad_rel <= 1e-10)}
 
 
 def config_dict(args, world, extra=None):
+    nb0, _, nb_total = lane_split(args, world, 0)
+    per = f"nb={nb0}/GPU" if args.scaling == "weak" else f"nb={nb_total} over {world} GPU(s) ({nb0} on rank 0)"
     d = {"workload": (f"C2 mass-damper-spring chain (SURVEY §8d): {args.n_unit} units (n={2 * args.n_unit}), "
-                      f"nb={args.nb}/GPU, nt={args.nt}, t_max={args.t_max}, backward Euler + discrete adjoint, "
+                      f"{per}, nt={args.nt}, t_max={args.t_max}, backward Euler + discrete adjoint, "
                       f"{args.solver} n_chunk={args.n_chunk}, Frobenius loss"),
-         "model": "mds", "n_unit": args.n_unit, "n_size": 2 * args.n_unit, "n_batch_per_gpu": args.nb,
-         "n_batch_total": args.nb * world, "n_time": args.nt, "n_chunk": args.n_chunk, "solver": args.solver,
-         "t_max": args.t_max, "parallelism": f"batch-sharded dp{world}",
-         "l2": "inputs larger than L2 (trajectory 1.6 GB/GPU, grid 80 MB), no flush"}
+         "model": "mds", "n_unit": args.n_unit, "n_size": 2 * args.n_unit, "n_batch_per_gpu": nb0,
+         "n_batch_total": nb_total, "n_time": args.nt, "n_chunk": args.n_chunk, "solver": args.solver,
+         "t_max": args.t_max, "parallelism": f"batch-sharded dp{world} ({args.scaling} scaling)",
+         "l2": (f"inputs larger than L2 (trajectory {8 * (args.nt + 1) * nb0 * 2 * args.n_unit / 1e9:.2f} GB/GPU), "
+                "no flush")}
     if extra:
         d.update(extra)
     return d
@@ -183,6 +223,19 @@ def config_dict(args, world, extra=None):
 # ---------------------------------------------------------------------------
 # reference arm: the compiled reference (oracle/_ref) on the host cores
 # ---------------------------------------------------------------------------
+def cpu_sample(args, world):
+    """The reference arms' bounded sample of the bench workload: every lane of the arm's config, the first
+    n_chunk steps of the full grid (same dt), solved with the same solver and n_chunk -- one full chunk of
+    the real configuration, so nothing is extrapolated but the step count."""
+    _, _, nb_total = lane_split(args, world, 0)
+    import paper_2310_08649_b200 as P
+    model = P.build_mass_damper_spring(args.n_unit, nb_total)
+    nt_s = args.cpu_sample_steps or args.n_chunk
+    times = uniform_times(nt_s, nb_total, args.t_max * nt_s / args.nt)
+    y0 = np.zeros((nb_total, model.state_size))
+    return model, y0, times, nt_s, min(args.n_chunk, nt_s)
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -191,10 +244,8 @@ def run_reference(args):
     kind = "reference" if ref_available() else "port"
     orc = load_ref() if kind == "reference" else load_port()
     cores = os.cpu_count() or 1
-    nt_s = args.cpu_sample_steps
-    model, y0, _ = mds_workload(args, 1, 0)
-    times = uniform_times(nt_s, args.nb, args.t_max * nt_s / args.nt)  # same dt as the full grid
-    nc = min(args.n_chunk, nt_s)
+    model, y0, times, nt_s, nc = cpu_sample(args, max(world, args.gpus))
+    nb = y0.shape[0]
     sv = (SOLVER_ID[args.solver], args.n_switch)
     secs = []
     for i in range(args.warmup + args.steps):
@@ -204,14 +255,16 @@ def run_reference(args):
         if i >= args.warmup:
             secs.append(s)
     sec = statistics.mean(secs)
-    v = args.nb * nt_s / sec
+    v = nb * nt_s / sec
     line = {"impl": "reference", "metric": "series*steps/s forward+adjoint (backward Euler, PCR)",
             "value": v, "unit": "series*steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args, 1, {"sample": f"nb={args.nb} x nt={nt_s} steps (dt as full grid)"}),
+            "config": config_dict(args, max(world, args.gpus),
+                                  {"sample": f"all {nb} lanes x the first {nt_s} steps (dt as the full grid), "
+                                             f"{args.solver} n_chunk={nc}"}),
             "cpu_baseline": {"value": v, "unit": "series*steps/s", "cores": cores, "kind": kind,
-                             "sample": f"nb={args.nb} lanes x {nt_s} steps per step, {cores} threads over "
+                             "sample": f"{nb} lanes x {nt_s} steps per step (n_chunk={nc}), {cores} threads over "
                                        f"contiguous lane shards (timing only: shard-local Newton predicate)"},
             "e2e": {"value": v, "unit": "series*steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -222,16 +275,14 @@ def cpu_baseline_single(args):
     from oracle import load_port, load_ref, ref_available
     kind = "reference" if ref_available() else "port"
     orc = load_ref() if kind == "reference" else load_port()
-    nt_s = args.cpu_sample_steps
-    model, y0, _ = mds_workload(args, 1, 0)
-    times = uniform_times(nt_s, args.nb, args.t_max * nt_s / args.nt)
-    nc = min(args.n_chunk, nt_s)
+    model, y0, times, nt_s, nc = cpu_sample(args, 1)
+    nb = y0.shape[0]
     t0 = time.perf_counter()
     orc.gradient(model, y0, times, nc, solver=(SOLVER_ID[args.solver], args.n_switch))
     sec = time.perf_counter() - t0
-    return {"value": args.nb * nt_s / sec, "unit": "series*steps/s", "cores": 1, "kind": kind,
-            "sample": f"nb={args.nb} lanes x first {nt_s} steps (same dt), single thread, forward+adjoint, "
-                      f"{sec:.1f} s"}
+    return {"value": nb * nt_s / sec, "unit": "series*steps/s", "cores": 1, "kind": kind,
+            "sample": f"all {nb} lanes x the first {nt_s} steps (same dt, n_chunk={nc}: one full chunk of the "
+                      f"workload), single thread, forward+adjoint, {sec:.1f} s"}
 
 
 def c3_pcr_vs_sequential(ctx, reps=2):
@@ -317,11 +368,26 @@ def c2_solver_family(args, local, nt_s=500, reps=2):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: re-run this script under torch.distributed.run with one
+    rank per GPU (the driver's own launch line), rendezvous on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     import torch
     import torch.distributed as dist
 
@@ -334,13 +400,17 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     model, y0, times = mds_workload(args, world, rank)
-    nb, nt, n = args.nb, args.nt, model.state_size
+    nb, nt, n = y0.shape[0], args.nt, model.state_size
+    _, _, nb_total = lane_split(args, world, rank)
     ctx = api.Context(local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     if world > 1:
         from paper_2310_08649_b200 import group
         group.join(ctx, rank, world)
+    print(json.dumps({"join": rank, "world": world, "device": local, "gpu": torch.cuda.get_device_name(local),
+                      "lanes": [model.lane_offset, model.lane_offset + nb], "n_batch_total": nb_total}),
+          file=sys.stderr, flush=True)
     L = lib()
     dm = ctx.model(model)
     d_y0 = torch.from_numpy(y0).cuda()
@@ -394,7 +464,7 @@ def main():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = nb * world * nt / (ms * 1e-3)
+    value = nb_total * nt / (ms * 1e-3)
 
     # ---- e2e: the public C ABI with pinned HOST buffers, H2D/D2H inside the timed region
     e2e = None
@@ -423,7 +493,7 @@ def main():
             t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        e2e = {"value": nb * world * nt / (e_ms * 1e-3), "unit": "series*steps/s",
+        e2e = {"value": nb_total * nt / (e_ms * 1e-3), "unit": "series*steps/s",
                "h2d_bytes_per_step": int(h_y0.numel() * 8 + h_times.numel() * 8),
                "d2h_bytes_per_step": int(grad.size * 8 + 8), "ms_per_step": e_ms,
                "path": "cko_gradient_adjoint (C ABI, pinned host y0/times -> loss + gradient)"}
@@ -456,7 +526,7 @@ def main():
     line = {
         "metric": "series*steps/s forward+adjoint (backward Euler, PCR)",
         "value": value, "unit": "series*steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference model parameters, uniform grid, y0 = 0)",
         "config": config_dict(args, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -470,6 +540,7 @@ def main():
         "newton": {"fwd": {kk: int(getattr(wf, kk)) for kk, _ in abi.CkoWork._fields_},
                    "bwd": {kk: int(getattr(wb, kk)) for kk, _ in abi.CkoWork._fields_}},
         "loss": loss.value,
+        "parity": golden_parity(args, nb_total, loss.value, grad, wf, wb),
         "gpu_launches": rec["launches"],
         "e2e": e2e,
     }

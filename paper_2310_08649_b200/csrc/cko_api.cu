@@ -313,6 +313,10 @@ cko_status cko_ctx_set_group(cko_ctx* c, int rank, int world, void* const* peers
   if (!c) return fail(err, CKO_ERROR, "null context");
   if (world < 1 || world > 8 || rank < 0 || rank >= world)
     return fail(err, CKO_ERROR, "cko_ctx_set_group: need 1 <= world <= 8, 0 <= rank < world");
+  if (world > 1) {  // no lazy module load may stall a rank while its peers spin on the exchange
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(preload_kernels());
+  }
   c->grp.rank = rank;
   c->grp.world = world;
   c->grp.red_cap = kRedCap;
@@ -593,6 +597,11 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   c->collect(0, 1);
   const int off = m->desc.lane_offset;
   if (info[0] == 4) return fail(err, CKO_COMM, "grid barrier timed out (device or peer stalled)");
+  if (info[0] == 1 && key == ~0ull) {  // FLAG_SINGULAR came from a peer rank through the group exchange
+    cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block on a peer rank of the batch group");
+    if (err) err->chunk_index = -1, err->batch_index = -1;
+    return s;
+  }
   if (info[0] == 1) {
     const int k = (int)(key / (unsigned long long)nb), b = (int)(key % (unsigned long long)nb);
     cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block at chunk row %d, batch %d", k, b + off);
@@ -682,7 +691,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   if (c->grp.world > 1 && np > c->grp.red_cap)
     return fail(err, CKO_COMM, "parameter count %d exceeds the group reduce buffer (%d)", np, c->grp.red_cap);
   CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm, nb, nt)));
-  CUDA_TRY(c->grad.ensure(sizeof(double) * np));
+  CUDA_TRY(c->grad.ensure(sizeof(double) * (np + 1)));  // + the group's singular-block flag
   CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
   c->last_launches = 3;
   c->last_gen = (nodep || v2 || p2) ? 2 : 1;
@@ -725,27 +734,29 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   CUDA_TRY(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),
                       c->grad.as<double>(), c->stream));
   if (c->grp.world > 1) {
-    CUDA_TRY(launch_group_sum(c->grp, c->gs.as<GridSync>(), c->grad.as<double>(), np, c->status.as<unsigned>(),
+    CUDA_TRY(launch_key_flag(c->key.as<unsigned long long>(), c->grad.as<double>() + np, c->stream));
+    CUDA_TRY(launch_group_sum(c->grp, c->gs.as<GridSync>(), c->grad.as<double>(), np + 1, c->status.as<unsigned>(),
                               c->stream));
-    c->last_launches += 1;
+    c->last_launches += 2;
   }
   c->mark(5);
   unsigned long long key;
   unsigned gstatus = 0;
   double L = NAN;
-  CUDA_TRY(c->pin.ensure(32 + sizeof(double) * (size_t)np));
+  CUDA_TRY(c->pin.ensure(32 + sizeof(double) * (size_t)(np + 1)));
   CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned>(0), c->status.p, sizeof gstatus, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(8), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
                            c->stream));
   if (loss_kind == CKO_LOSS_FROBENIUS)
     CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(16), c->loss.p, sizeof L, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(32), c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost,
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(32), c->grad.p, sizeof(double) * (np + 1), cudaMemcpyDeviceToHost,
                            c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   gstatus = *c->pin.as<unsigned>(0);
   key = *c->pin.as<unsigned long long>(8);
   if (loss_kind == CKO_LOSS_FROBENIUS) L = *c->pin.as<double>(16);
   std::memcpy(grad_out, c->pin.as<double>(32), sizeof(double) * np);
+  const bool group_singular = c->grp.world > 1 && c->pin.as<double>(32)[np] > 0.0;
   c->last_ms[0] = 0.0;
   c->collect(1, 3);
   if (gstatus) return fail(err, CKO_COMM, "group reduction timed out (peer stalled)");
@@ -755,6 +766,11 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
     const int r = (int)((key / (unsigned long long)nb) % (unsigned long long)nc);
     cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular diagonal block at chunk row %d, batch %d", r, b + off);
     if (err) err->chunk_index = r, err->batch_index = b + off;
+    return s;
+  }
+  if (group_singular) {
+    cko_status s = fail(err, CKO_SINGULAR_BLOCK, "singular adjoint block on a peer rank of the batch group");
+    if (err) err->chunk_index = -1, err->batch_index = -1;
     return s;
   }
   for (int j = 0; j < np; ++j)

@@ -6,20 +6,44 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace cko {
 
-// Raise a kernel's dynamic shared-memory limit to 226 KB (227 KB minus the static
-// part) once per
-// process (thread-safe static init). Setting it on every launch would
-// serialise concurrent launches of the same kernel from other streams: the
-// attribute write waits for running instances.
-#define CKO_ALLOW_FULL_SMEM(KERNEL)                                                                    \
-  do {                                                                                                \
-    static const cudaError_t _cko_attr_err = cudaFuncSetAttribute(                                    \
-        (const void*)(KERNEL), cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);              \
-    if (_cko_attr_err != cudaSuccess) return _cko_attr_err;                                           \
+// Raise a kernel's dynamic shared-memory limit. Function attributes live in
+// each device's context, so the setting is cached per (device, kernel): a
+// second context on another device sets it again. Setting it on every launch
+// would serialise concurrent launches of the same kernel from other streams
+// (the attribute write waits for running instances).
+inline cudaError_t allow_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({dev, func});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[{dev, func}] = bytes;
+  return e;
+}
+// Force a kernel's module to load now. With lazy module loading (the CUDA 12
+// default) the first launch of a kernel may wait for the device to go idle;
+// in a batch group a rank whose host thread blocks there while its peer's
+// kernel spins on the group exchange would stall both. cko_ctx_set_group
+// therefore loads every kernel up front.
+inline cudaError_t preload(const void* func) {
+  cudaFuncAttributes fa;
+  return cudaFuncGetAttributes(&fa, func);
+}
+#define CKO_ALLOW_FULL_SMEM(KERNEL)                                                   \
+  do {                                                                               \
+    const cudaError_t _cko_attr_err = ::cko::allow_smem((const void*)(KERNEL), 226 * 1024); \
+    if (_cko_attr_err != cudaSuccess) return _cko_attr_err;                          \
   } while (0)
 
 // Persistent grid-barrier kernels launch cooperatively (every CTA resident).

@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(256) vjp_kernel(DevModel m, const double* stat
 #define CKO_DECLARE(NAME)                                                                       \
   cudaError_t fwd_run_##NAME(const FwdLaunch& a, cudaStream_t st);                                 \
   cudaError_t fwd_occ_##NAME(int threads, int* blocks);                                            \
+  cudaError_t preload_##NAME();                                                                    \
   cudaError_t adj_run_##NAME(const AdjLaunch& a, cudaStream_t st);                                 \
   cudaError_t vjp_run_##NAME(const DevModel& m, const double* states, const double* times,          \
                              const double* wq, int nb, int nt, double* scratch, cudaStream_t st);

@@ -15,6 +15,13 @@
   cudaError_t fwd_occ_##NAME(int threads, int* blocks) {                                              \
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fwd_kernel<MD>, threads, 0);         \
   }                                                                                                   \
+  cudaError_t preload_##NAME() {                                                                      \
+    for (const void* f : {(const void*)fwd_kernel<MD>, (const void*)adj_kernel<MD>,                   \
+                          (const void*)vjp_kernel<MD, 16>, (const void*)vjp_kernel<MD, 64>,           \
+                          (const void*)vjp_kernel<MD, 1024>})                                         \
+      if (cudaError_t e = preload(f)) return e;                                                       \
+    return cudaSuccess;                                                                               \
+  }                                                                                                   \
   cudaError_t adj_run_##NAME(const AdjLaunch& a, cudaStream_t st) {                                   \
     adj_kernel<MD><<<a.grid, a.threads, 0, st>>>(a);                                                  \
     return cudaGetLastError();                                                                        \

@@ -133,6 +133,15 @@ __global__ void group_sum_kernel(GroupView g, GridSync* gs, double* v, int cnt, 
   group_sum_block(g, gs, v, cnt, v, budget_ns, status);
 }
 
+// v[0] = 1 when this rank's adjoint found a singular block (its key is set): summed with the gradient so a
+// peer learns that another shard failed and reports it instead of returning a partial gradient.
+__global__ void key_flag_kernel(const unsigned long long* key, double* v) { *v = *key != ~0ull ? 1.0 : 0.0; }
+
+cudaError_t launch_key_flag(const unsigned long long* key, double* v, cudaStream_t st) {
+  key_flag_kernel<<<1, 1, 0, st>>>(key, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cnt, unsigned* status, cudaStream_t st) {
   group_sum_kernel<<<1, 256, 0, st>>>(g, gs, v, cnt, 60ull * 1000 * 1000 * 1000, status);
   return cudaGetLastError();
@@ -215,6 +224,26 @@ cudaError_t launch_adjoint_pcr2(int kind, int n, const AdjLaunch* a, cudaStream_
 #define CALL(N) adjp_run_##N(n, a, st)
   CKO_SWITCH(kind, CALL)
 #undef CALL
+}
+
+// Load every kernel of the library on the current device (see cko::preload).
+cudaError_t preload_kernels() {
+#define CALL(N) preload_##N()
+  for (int kind = 0; kind <= 5; ++kind) {
+    cudaError_t e = [&]() -> cudaError_t { CKO_SWITCH(kind, CALL) }();
+    if (e != cudaSuccess) return e;
+    for (int n = 1; n <= 32; ++n) {  // the specialised kernels' probes load them (NotSupported: none for n)
+      for (cudaError_t p : {launch_forward_v2(kind, n, nullptr, nullptr), launch_adjoint_v2(kind, n, nullptr, nullptr),
+                            launch_forward_pcr2(kind, n, nullptr, nullptr),
+                            launch_adjoint_pcr2(kind, n, nullptr, nullptr)})
+        if (p != cudaSuccess && p != cudaErrorNotSupported) return p;
+    }
+  }
+#undef CALL
+  for (const void* f : {(const void*)solve_kernel, (const void*)loss_partial_kernel, (const void*)loss_final_kernel,
+                        (const void*)group_sum_kernel, (const void*)key_flag_kernel, (const void*)vjp_final_kernel})
+    if (cudaError_t e = preload(f)) return e;
+  return preload_node_kernels();
 }
 
 cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st) {

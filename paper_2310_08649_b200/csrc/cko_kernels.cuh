@@ -105,6 +105,9 @@ inline int pcr2_ws_bound(int n) { return 3 * n * n + 5 * n + 20; }
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
                         const GroupView& g, GridSync* gs, unsigned* status, cudaStream_t st);
 // In-place deterministic sum of v[0..cnt) over the ranks of the group.
+cudaError_t preload_kernels();
+cudaError_t preload_node_kernels();
+cudaError_t launch_key_flag(const unsigned long long* key, double* v, cudaStream_t st);
 cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cnt, unsigned* status,
                              cudaStream_t st);
 // grad (device, np) = sum over (m >= 1, b) of w . dh/dp; scratch sized by vjp_scratch_doubles.

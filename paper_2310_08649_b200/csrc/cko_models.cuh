@@ -86,10 +86,10 @@ struct MLin3 {
     const double y0 = y[0], y1 = y[1], y2 = y[2];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      double acc = p[3 * i] * y0;
-      acc += p[3 * i + 1] * y1;
-      acc += p[3 * i + 2] * y2;
-      if (i == 0) acc += p[9] * sin(CKO_TWO_PI * t / m.periods[m.off + b]);
+      double acc = xmul(p[3 * i], y0);
+      acc = xadd(acc, xmul(p[3 * i + 1], y1));
+      acc = xadd(acc, xmul(p[3 * i + 2], y2));
+      if (i == 0) acc = xadd(acc, xmul(p[9], sin(CKO_TWO_PI * t / m.periods[m.off + b])));
       out[i] = acc;
     }
   }
@@ -122,12 +122,13 @@ struct MMds {
     for (int u = 0; u < n; ++u) out[u] = y[n + u];
     for (int u = 0; u < n; ++u) {
       double acc = 0.0;
+      // no contraction: the reference's separately rounded products and sums
       if (u > 0)
-        acc += (K[u] / M[u]) * (y[u] - y[u - 1]) + (C[u] / M[u]) * (y[n + u] - y[n + u - 1]);
+        acc = xadd(acc, xadd(xmul(K[u] / M[u], y[u] - y[u - 1]), xmul(C[u] / M[u], y[n + u] - y[n + u - 1])));
       if (u + 1 < n)
-        acc -= (K[u + 1] / M[u + 1]) * (y[u + 1] - y[u]) +
-               (C[u + 1] / M[u + 1]) * (y[n + u + 1] - y[n + u]);
-      if (u == 0) acc += fa * sin(CKO_TWO_PI * t / Tb);
+        acc = xsub(acc, xadd(xmul(K[u + 1] / M[u + 1], y[u + 1] - y[u]),
+                             xmul(C[u + 1] / M[u + 1], y[n + u + 1] - y[n + u])));
+      if (u == 0) acc = xadd(acc, xmul(fa, sin(CKO_TWO_PI * t / Tb)));
       out[n + u] = acc;
     }
   }
@@ -197,9 +198,10 @@ struct MChaboche {
     const double ramp = pow_value(over > 0.0 ? over : 0.0, nn);
     const double ep = ramp * sg;
     const double ep_abs = ramp * (sg * sg);
-    out[0] = E * (ea * sin(CKO_TWO_PI * t / Tp) - ep);
+    out[0] = xmul(E, xsub(xmul(ea, sin(CKO_TWO_PI * t / Tp)), ep));
     out[1] = tau * (Kinf - K);
-    for (int i = 0; i < n; ++i) out[2 + i] = (2.0 / 3.0) * C[i] * ep - gam[i] * y[2 + i] * ep_abs;
+    for (int i = 0; i < n; ++i)
+      out[2 + i] = xsub(xmul(xmul(2.0 / 3.0, C[i]), ep), xmul(xmul(gam[i], y[2 + i]), ep_abs));
   }
   template <class Y, class J>
   __device__ static void jacobian(const DevModel& m, double, const Y& y, J& jac, int) {
@@ -223,11 +225,12 @@ struct MChaboche {
     for (int i = 0; i < n; ++i) {
       const double Xi = y[2 + i];
       const double ci = (2.0 / 3.0) * C[i];
-      jac(2 + i, 0) = ci * D * sg2 - gam[i] * Xi * D * sg;
-      jac(2 + i, 1) = -ci * D * sg + gam[i] * Xi * D * sg2;
-      const double v = -ci * D * sg2 + gam[i] * Xi * D * sg;
+      const double gX = xmul(gam[i], Xi);
+      jac(2 + i, 0) = xsub(xmul(xmul(ci, D), sg2), xmul(xmul(gX, D), sg));
+      jac(2 + i, 1) = xadd(xmul(xmul(-ci, D), sg), xmul(xmul(gX, D), sg2));
+      const double v = xadd(xmul(xmul(-ci, D), sg2), xmul(xmul(gX, D), sg));
       for (int j = 0; j < n; ++j) jac(2 + i, 2 + j) = v;
-      jac(2 + i, 2 + i) = v - gam[i] * ramp * sg2;
+      jac(2 + i, 2 + i) = xsub(v, xmul(xmul(gam[i], ramp), sg2));
     }
   }
   template <class Y, class Wt, class G>
@@ -296,17 +299,17 @@ struct MNode {
     z0[n] = sin(CKO_TWO_PI * t / m.periods[m.off + b]);
     for (int i = 0; i < W; ++i) {
       double acc = b1[i];
-      for (int j = 0; j < w0; ++j) acc += W1[i * w0 + j] * z0[j];
+      for (int j = 0; j < w0; ++j) acc = xadd(acc, xmul(W1[i * w0 + j], z0[j]));
       z1[i] = tanh(acc);
     }
     for (int i = 0; i < W; ++i) {
       double acc = b2[i];
-      for (int j = 0; j < W; ++j) acc += W2[i * W + j] * z1[j];
+      for (int j = 0; j < W; ++j) acc = xadd(acc, xmul(W2[i * W + j], z1[j]));
       z2[i] = tanh(acc);
     }
     for (int i = 0; i < n; ++i) {
       double acc = b3[i];
-      for (int j = 0; j < W; ++j) acc += W3[i * W + j] * z2[j];
+      for (int j = 0; j < W; ++j) acc = xadd(acc, xmul(W3[i * W + j], z2[j]));
       o[i] = tanh(acc);
     }
   }

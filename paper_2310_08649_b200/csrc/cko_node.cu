@@ -240,7 +240,7 @@ constexpr int kRec = N * N + N + 6;  // LU | 1/U_ii | perm (N + 1 ints) — 16-b
 // dL + dt J^T lambda) and factor it (lu_factor_block rule).
 __global__ void node_factor_kernel(const double* J, const double* times, int step_or_hi, int c, int nb,
                                    int adjoint, double* recs, unsigned long long* sing_key, unsigned long long ord,
-                                   int nc) {
+                                   int nc, unsigned* flags) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c * nb; p += gridDim.x * blockDim.x) {
     const int k = p / nb, b = p % nb;
     const int m = adjoint ? step_or_hi - k : step_or_hi + 1 + k;
@@ -282,9 +282,11 @@ __global__ void node_factor_kernel(const double* J, const double* times, int ste
 #pragma unroll
     for (int e = 0; e < N * N + N; e += 2)
       *reinterpret_cast<double2*>(rec + e) = make_double2(loc[e], loc[e + 1]);
-    if (!ok)
+    if (!ok) {
       atomicMin(sing_key, adjoint ? ord * (unsigned long long)nc * nb + (unsigned long long)k * nb + b
                                   : (unsigned long long)k * nb + b);
+      if (flags) atomicOr(flags, FLAG_SINGULAR);  // reaches the peers through the group flag exchange
+    }
   }
 }
 
@@ -613,15 +615,22 @@ __global__ void __launch_bounds__(kVecThreads) node_vectors_dmma_kernel(DevModel
 
 cudaError_t launch_node_vectors_dmma(const DevModel& m, const double* states, const double* times, const double* wq,
                                      int nb, size_t P, double* vec, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(node::node_vectors_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         node::kVecSmem);
-    attr = true;
-  }
+  const cudaError_t attr = allow_smem((const void*)node::node_vectors_dmma_kernel, node::kVecSmem);
+  if (attr != cudaSuccess) return attr;
   node::node_vectors_dmma_kernel<<<2 * 148, node::kVecThreads, node::kVecSmem, st>>>(m, states, times, wq, nb, P,
                                                                                       vec);
   return cudaGetLastError();
+}
+
+cudaError_t preload_node_kernels() {
+  using namespace node;
+  for (const void* f : {(const void*)node_eval_kernel, (const void*)node_residual_kernel,
+                        (const void*)node_residual_pp_kernel, (const void*)node_factor_kernel,
+                        (const void*)node_thomas_fwd_kernel, (const void*)node_adj_rhs_kernel,
+                        (const void*)node_thomas_adj_kernel, (const void*)node_init_chunk_kernel,
+                        (const void*)node_group_flags_kernel, (const void*)node_vectors_dmma_kernel})
+    if (cudaError_t e = preload(f)) return e;
+  return cudaSuccess;
 }
 
 bool node_fast_path(const DevModel& m) { return m.kind == 5 && m.n == node::N && m.W == node::W; }
@@ -633,8 +642,7 @@ size_t node_scratch_doubles(int nb, int c) {
 
 cudaError_t node_eval(const DevModel& m, const double* states, const double* times, int row0, int dir, int nb,
                       int P, double* H, double* J, bool want_j, cudaStream_t st) {
-  static const cudaError_t attr = cudaFuncSetAttribute((const void*)node::node_eval_kernel,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, node::kEvalSmem);
+  const cudaError_t attr = allow_smem((const void*)node::node_eval_kernel, node::kEvalSmem);
   if (attr != cudaSuccess) return attr;
   const int tiles = (P + node::TP - 1) / node::TP;
   node::node_eval_kernel<<<tiles < 2 * 148 ? tiles : 2 * 148, node::kEvalThreads, node::kEvalSmem, st>>>(
@@ -695,13 +703,13 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
       if (it == max_iter) return info[0] = 2, info[1] = step + 1, info[2] = max_iter, cudaSuccess;
       ++it;
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
-      node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step, c, nb, 0, recs, sing_key, 0, nc);
-      static const cudaError_t fattr = cudaFuncSetAttribute(
-          (const void*)node_thomas_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubSmem);
+      if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+      node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step, c, nb, 0, recs, sing_key, 0, nc,
+                                                               d_flags);
+      const cudaError_t fattr = allow_smem((const void*)node_thomas_fwd_kernel, kSubSmem);
       if (fattr != cudaSuccess) return fattr;
       node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(states, R, recs, step, c, nb);
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
-      if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
       launch_node_residual(states, times, H, step, c, nb, R, r0, rn, 0, tol_a, tol_r, d_flags, st);
       if ((e = flags(f)) != cudaSuccess) return e;
       unsigned long long key = ~0ull;
@@ -710,7 +718,8 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
       std::memcpy(&key, h_flags + 2, sizeof key);
       if (f & FLAG_TIMEOUT) return info[0] = 4, cudaSuccess;
-      if (key != ~0ull) return info[0] = 1, info[1] = step + 1, info[2] = it, cudaSuccess;
+      // FLAG_SINGULAR with no local key: the singular block sits on a peer rank
+      if (key != ~0ull || (f & FLAG_SINGULAR)) return info[0] = 1, info[1] = step + 1, info[2] = it, cudaSuccess;
       if (f & FLAG_NON_FINITE) return info[0] = 2, info[1] = step + 1, info[2] = it, cudaSuccess;
     }
     iters[chunk] = it;
@@ -743,9 +752,9 @@ cudaError_t node_adjoint(const DevModel& m, const double* states, const double* 
     // row r of the chunk is trajectory step step_hi - r
     if ((e = node_eval(m, states, times, step_hi, -1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
     node_adj_rhs_kernel<<<blocks_for(P, 128), 128, 0, st>>>(states, times, Jb, dL, loss, lam, step_hi, c, nb, R);
-    node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step_hi, c, nb, 1, recs, sing_key, ord, nc);
-    static const cudaError_t aattr = cudaFuncSetAttribute(
-        (const void*)node_thomas_adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSubSmem);
+    node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step_hi, c, nb, 1, recs, sing_key, ord, nc,
+                                                             nullptr);
+    const cudaError_t aattr = allow_smem((const void*)node_thomas_adj_kernel, kSubSmem);
     if (aattr != cudaSuccess) return aattr;
     node_thomas_adj_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(R, recs, times, step_hi, c,
                                                                                         nb, lam, wq);

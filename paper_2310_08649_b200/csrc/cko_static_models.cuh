@@ -65,11 +65,13 @@ struct MdsS {
     for (int u = 0; u < NU; ++u) h[u] = y[NU + u];
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
+      // no contraction: the reference's separately rounded products and sums
       double acc = 0.0;
-      if (u > 0) acc += cs[u] * (y[u] - y[u - 1]) + cs[NU + u] * (y[NU + u] - y[NU + u - 1]);
+      if (u > 0)
+        acc = xadd(acc, xadd(xmul(cs[u], y[u] - y[u - 1]), xmul(cs[NU + u], y[NU + u] - y[NU + u - 1])));
       if (u + 1 < NU)
-        acc -= cs[u + 1] * (y[u + 1] - y[u]) + cs[NU + u + 1] * (y[NU + u + 1] - y[NU + u]);
-      if (u == 0) acc += cs[2 * NU] * sin(CKO_TWO_PI * t / Tb);
+        acc = xsub(acc, xadd(xmul(cs[u + 1], y[u + 1] - y[u]), xmul(cs[NU + u + 1], y[NU + u + 1] - y[NU + u])));
+      if (u == 0) acc = xadd(acc, xmul(cs[2 * NU], sin(CKO_TWO_PI * t / Tb)));
       h[NU + u] = acc;
     }
   }
@@ -128,10 +130,10 @@ struct Lin3S {
                               int b) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      double acc = cs[3 * i] * y[0];
-      acc += cs[3 * i + 1] * y[1];
-      acc += cs[3 * i + 2] * y[2];
-      if (i == 0) acc += cs[9] * sin(CKO_TWO_PI * t / m.periods[m.off + b]);
+      double acc = xmul(cs[3 * i], y[0]);
+      acc = xadd(acc, xmul(cs[3 * i + 1], y[1]));
+      acc = xadd(acc, xmul(cs[3 * i + 2], y[2]));
+      if (i == 0) acc = xadd(acc, xmul(cs[9], sin(CKO_TWO_PI * t / m.periods[m.off + b])));
       h[i] = acc;
     }
   }
@@ -167,10 +169,10 @@ struct ChabS {
     const double ramp = pow_value(over > 0.0 ? over : 0.0, nn);
     const double ep = ramp * sg;
     const double ep_abs = ramp * (sg * sg);
-    h[0] = E * (ea * sin(CKO_TWO_PI * t / Tp) - ep);
+    h[0] = xmul(E, xsub(xmul(ea, sin(CKO_TWO_PI * t / Tp)), ep));
     h[1] = tau * (Kinf - K);
 #pragma unroll
-    for (int i = 0; i < NU; ++i) h[2 + i] = (2.0 / 3.0) * C[i] * ep - gam[i] * y[2 + i] * ep_abs;
+    for (int i = 0; i < NU; ++i) h[2 + i] = xsub(xmul(xmul(2.0 / 3.0, C[i]), ep), xmul(xmul(gam[i], y[2 + i]), ep_abs));
   }
   __device__ static void jac_row(const DevModel&, const double* cs, double, const double (&y)[N], int i,
                                  double (&row)[N], int) {
@@ -200,11 +202,12 @@ struct ChabS {
 #pragma unroll
       for (int q = 0; q < NU; ++q)
         if (i == 2 + q) ci = (2.0 / 3.0) * C[q], gi = gam[q], Xi = y[2 + q];
-      row[0] = ci * D * sg2 - gi * Xi * D * sg;
-      row[1] = -ci * D * sg + gi * Xi * D * sg2;
-      const double v = -ci * D * sg2 + gi * Xi * D * sg;
+      const double gX = xmul(gi, Xi);
+      row[0] = xsub(xmul(xmul(ci, D), sg2), xmul(xmul(gX, D), sg));
+      row[1] = xadd(xmul(xmul(-ci, D), sg), xmul(xmul(gX, D), sg2));
+      const double v = xadd(xmul(xmul(-ci, D), sg2), xmul(xmul(gX, D), sg));
 #pragma unroll
-      for (int j = 0; j < NU; ++j) row[2 + j] = (i == 2 + j) ? v - gi * ramp * sg2 : v;
+      for (int j = 0; j < NU; ++j) row[2 + j] = (i == 2 + j) ? xsub(v, xmul(xmul(gi, ramp), sg2)) : v;
     }
   }
 };

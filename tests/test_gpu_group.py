@@ -43,13 +43,10 @@ def _group(ctxs):
 
 
 def _run_group(full, nb_local, world, y0, t_local, nc, solver):
-    # Two ranks emulated on ONE GPU depend on both grids being scheduled together; a rare scheduling stall
-    # shows up as the kernels' bounded barrier timeout (a DeviceError, never a hang). One retry on a fresh
-    # group; a real protocol error fails both attempts.
-    try:
-        return _run_group_once(full, nb_local, world, y0, t_local, nc, solver)
-    except P.DeviceError:
-        return _run_group_once(full, nb_local, world, y0, t_local, nc, solver)
+    # No retry: the one-GPU emulation used to stall when a rank's host thread launched a group-only kernel
+    # for the first time (lazy module loading waits for the device while the peer kernel spins on the
+    # exchange). cko_ctx_set_group now loads every kernel up front (cko::preload_kernels).
+    return _run_group_once(full, nb_local, world, y0, t_local, nc, solver)
 
 
 def _run_group_once(full, nb_local, world, y0, t_local, nc, solver):

@@ -93,3 +93,20 @@ def test_port_matches_reference_live(port, ref):
         assert a.fwd == b.fwd and a.bwd == b.bwd
         assert rel_max(a.states, b.states) <= 1e-13
         assert rel_max(a.grad, b.grad) <= 1e-12
+
+
+@pytest.mark.parametrize("prefix,nc,solver", [("seq_", 1, (0, 1)), ("pcr256_", 256, (1, 1))])
+def test_port_matches_reference_full_c3(port, prefix, nc, solver):
+    """C3 at full size (nb = 50, nt = 20000): the restatement against the reference's own run
+    (tests/golden/full_c3.npz), so the GPU's full-size check inherits a pinned chain."""
+    from tests.cases import chaboche_plastic
+    from tests.conftest import uniform_times
+    g = np.load(os.path.join(GOLD, "full_c3.npz"))
+    nb, nt = int(g["nb"]), int(g["nt"])
+    m = chaboche_plastic(int(g["n_unit"]), nb, float(g["eps_scale"]))
+    r = port.gradient(m, np.zeros((nb, m.state_size)), uniform_times(nt, nb, float(g["t_max"])), nc, solver=solver)
+    assert [r.fwd[k] for k in KEYS] == list(g[prefix + "fwd"])
+    assert [r.bwd[k] for k in KEYS] == list(g[prefix + "bwd"])
+    assert abs(r.loss - float(g[prefix + "loss"])) <= 1e-13 * abs(float(g[prefix + "loss"]))
+    assert rel_max(r.grad, g[prefix + "grad"]) <= 1e-12
+    assert rel_max(r.states[-1], g[prefix + "last_row"]) <= 1e-13
