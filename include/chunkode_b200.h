@@ -215,6 +215,21 @@ cko_status cko_traj_states(const cko_traj* traj, const double** d_states, int* n
                            int* n);
 cko_status cko_traj_destroy(cko_traj* traj);
 
+/* ---- forward Euler scheme ----------------------------- */
+/* integrate_forward_euler (integrate.hpp:91-96, integrate.cpp:371-407): host y0 (nb, n),
+ * times (nt+1, nb) -> states_out (nt+1, nb*n); strictly step-sequential, so the result
+ * does not depend on n_chunk (>= 1). A non-finite state -> CKO_NON_FINITE naming the step.
+ * `work` receives rate_evals = nt. */
+cko_status cko_fe_forward(cko_ctx* ctx, const cko_model* model, const double* y0, const double* times, int nb,
+                          int nt, int n_chunk, double* states_out, cko_work* work, cko_error* err);
+
+/* adjoint_backward(..., Scheme::forward_euler, ...) (adjoint.hpp:63-66, adjoint.cpp:157-188)
+ * over a HOST trajectory; arguments as cko_be_adjoint_host. No linear solves: the backward
+ * counters carry one Jacobian evaluation per chunk. */
+cko_status cko_fe_adjoint_host(cko_ctx* ctx, const cko_model* model, const double* states, const double* times,
+                               int nb, int nt, int n_chunk, int loss_kind, const double* dL_host,
+                               double* loss_out, double* grad_out, cko_work* bwd, cko_error* err);
+
 /* ---- block-bidiagonal solver -------------------------------------------- */
 /* solve_thomas / solve_pcr / solve_hybrid (linalg.hpp:55-81,
  * linalg.cpp:307-344): diag (nc, nb, n, n), offdiag (nc-1, nb, n, n) or NULL
@@ -225,14 +240,50 @@ cko_status cko_block_bidiag_solve(cko_ctx* ctx, const cko_solver_choice* solver,
                                   int n, const double* diag, const double* offdiag,
                                   double* rhs_inout, long long* sweeps, cko_error* err);
 
-/* ---- single-chunk ops (integrate.hpp:53-77) ------------------------------ */
-/* newton_solve_chunk: dy (c, nb, n) in/out, y_start (nb, n), t_chunk and
- * dt_chunk (c, nb); returns the iteration count in *iterations. */
+/* ---- single-chunk ops (integrate.hpp:53-77, adjoint.hpp:36-56) ------------ */
+/* Kernel-level parity points; they run the generic (generation 1) kernels.
+ *
+ * newton_solve_chunk (integrate.hpp:63-67, integrate.cpp:299-319): dy (c, nb, n)
+ * in/out, y_start (nb, n), t_chunk and dt_chunk (c, nb) used as given (dt_chunk
+ * need not be the differences of t_chunk); returns the iteration count in
+ * *iterations; `work` receives this call's counters. */
 cko_status cko_newton_solve_chunk(cko_ctx* ctx, const cko_model* model, const double* y_start,
                                   double* dy, const double* t_chunk, const double* dt_chunk,
                                   int c, int nb, const cko_newton_settings* settings,
                                   const cko_solver_choice* solver, int chunk_start_step,
                                   int* iterations, cko_work* work, cko_error* err);
+
+/* chunk_residual (integrate.hpp:53-55, integrate.cpp:269-278):
+ * out(j) = dy(j) - dy(j-1) - h(y_start + dy(j), t_chunk(j)) dt_chunk(j), out (c, nb, n).
+ * A non-finite rate -> CKO_NON_FINITE (NonFiniteOutput). */
+cko_status cko_chunk_residual(cko_ctx* ctx, const cko_model* model, const double* y_start, const double* dy,
+                              const double* t_chunk, const double* dt_chunk, int c, int nb, double* out,
+                              cko_error* err);
+
+/* chunk_jacobian (integrate.hpp:57-61, integrate.cpp:280-297), analytic Jacobian:
+ * diag_out (c, nb, n, n) = I - J(y_start + dy(j), t_chunk(j)) dt_chunk(j); offdiag_out
+ * (c-1, nb, n, n) = -I (may be NULL). A non-finite J -> CKO_NON_FINITE. */
+cko_status cko_chunk_jacobian(cko_ctx* ctx, const cko_model* model, const double* y_start, const double* dy,
+                              const double* t_chunk, const double* dt_chunk, int c, int nb, double* diag_out,
+                              double* offdiag_out, cko_error* err);
+
+/* adjoint_chunk_solve (adjoint.hpp:49-56, adjoint.cpp:246-261) over a HOST trajectory
+ * states (nt+1, nb*n), times (nt+1, nb) and loss gradient dL (nt+1, nb*n): reverses
+ * steps step_hi - chunk_len + 1 .. step_hi in one coupled solve. lambda (nb, n) is the
+ * AdjointState carry (in/out); grad (np) accumulates the chunk's quadrature. `work`
+ * receives this call's counters (one Jacobian evaluation, one solve, its sweeps). */
+cko_status cko_adjoint_chunk_solve(cko_ctx* ctx, const cko_model* model, const double* states,
+                                   const double* times, int nb, int nt, int step_hi, int chunk_len,
+                                   const double* dL, const cko_solver_choice* solver, double* lambda,
+                                   double* grad, cko_work* work, cko_error* err);
+
+/* adjoint_step_sequential (adjoint.hpp:36-47, adjoint.cpp:223-244): one reverse step
+ * with y_i, y_prev, dL_i (nb, n) and t_i, t_prev (nb); t_i > t_prev per lane, else
+ * CKO_SHAPE_MISMATCH. lambda (nb, n) in/out, grad (np) accumulates. */
+cko_status cko_adjoint_step_sequential(cko_ctx* ctx, const cko_model* model, const double* y_i,
+                                       const double* y_prev, const double* t_i, const double* t_prev,
+                                       const double* dL_i, int nb, const cko_solver_choice* solver,
+                                       double* lambda, double* grad, cko_error* err);
 
 /* ---- measurement ----------------------------------------------------------- */
 /* Record CUDA events around every kernel launch on the context stream;

@@ -189,6 +189,73 @@ class Oracle:
         raise_for(rc, e)
         return x
 
+    # -- forward Euler scheme (reference only) ----------------------------------
+    def fe_gradient(self, model, y0, times, n_chunk, dL=None):
+        assert self.kind == "ref"
+        y0 = np.ascontiguousarray(y0, np.float64)
+        times = np.ascontiguousarray(times, np.float64)
+        nt, nb = times.shape[0] - 1, times.shape[1]
+        states = np.zeros((nt + 1, nb * model.state_size))
+        wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+        d = model.desc()
+        self.lib.ref_fe_forward.restype = C.c_int
+        self.lib.ref_fe_adjoint.restype = C.c_int
+        raise_for(self.lib.ref_fe_forward(C.byref(d), dptr(y0), dptr(times), nb, nt, n_chunk, dptr(states),
+                                          C.byref(wf), C.byref(e)), e)
+        grad = np.zeros(model.params.size)
+        L = C.c_double(0.0)
+        kind = abi.CKO_LOSS_FROBENIUS if dL is None else abi.CKO_LOSS_USER
+        dLa = None if dL is None else np.ascontiguousarray(dL, np.float64)
+        raise_for(self.lib.ref_fe_adjoint(C.byref(d), dptr(states), dptr(times), nb, nt, n_chunk, kind, dptr(dLa),
+                                          C.byref(L), dptr(grad), C.byref(wb), C.byref(e)), e)
+        return Result(states=states, loss=L.value, grad=grad, fwd=work_dict(wf), bwd=work_dict(wb))
+
+    # -- public single-chunk ops (reference only) --------------------------------
+    def chunk_op(self, model, op, y_start, dy, t_chunk, dt_chunk, settings=(1e-8, 1e-6, 100), solver=(0, 1)):
+        """op 0 chunk_residual -> r; 1 chunk_jacobian -> (diag, offdiag); 2 newton_solve_chunk ->
+        (dy, iterations, work)."""
+        assert self.kind == "ref"
+        y_start = np.ascontiguousarray(y_start, np.float64)
+        dy = np.ascontiguousarray(dy, np.float64).copy()
+        t_chunk = np.ascontiguousarray(t_chunk, np.float64)
+        dt_chunk = np.ascontiguousarray(dt_chunk, np.float64)
+        c, nb, n = dy.shape
+        out = np.zeros((c, nb, n) if op == 0 else (c, nb, n, n))
+        out2 = np.zeros((max(c - 1, 0), nb, n, n))
+        st, sv = abi.CkoNewtonSettings(*settings), abi.CkoSolverChoice(*solver)
+        it = C.c_int(0)
+        w, e = abi.CkoWork(), abi.CkoError()
+        d = model.desc()
+        self.lib.ref_chunk_op.restype = C.c_int
+        rc = self.lib.ref_chunk_op(C.byref(d), op, dptr(y_start), dptr(dy), dptr(t_chunk), dptr(dt_chunk), c, nb,
+                                   C.byref(st), C.byref(sv), dptr(out), dptr(out2), C.byref(it), C.byref(w),
+                                   C.byref(e))
+        raise_for(rc, e)
+        if op == 0:
+            return out
+        if op == 1:
+            return out, out2
+        return dy, int(it.value), work_dict(w)
+
+    def adjoint_chunk(self, model, op, states, times, step_hi, chunk_len, dL, lam, grad, solver=(0, 1)):
+        """op 0 adjoint_chunk_solve over (states, times, dL); op 1 adjoint_step_sequential with
+        states/times/dL = 2-row [prev; i] arrays. Returns (lambda, grad, work)."""
+        assert self.kind == "ref"
+        states = np.ascontiguousarray(states, np.float64)
+        times = np.ascontiguousarray(times, np.float64)
+        dL = np.ascontiguousarray(dL, np.float64)
+        lam = np.ascontiguousarray(lam, np.float64).copy()
+        grad = np.ascontiguousarray(grad, np.float64).copy()
+        nt, nb = times.shape[0] - 1, times.shape[1]
+        sv = abi.CkoSolverChoice(*solver)
+        w, e = abi.CkoWork(), abi.CkoError()
+        d = model.desc()
+        self.lib.ref_adjoint_chunk.restype = C.c_int
+        rc = self.lib.ref_adjoint_chunk(C.byref(d), op, dptr(states), dptr(times), nb, nt, step_hi, chunk_len,
+                                        dptr(dL), C.byref(sv), dptr(lam), dptr(grad), C.byref(w), C.byref(e))
+        raise_for(rc, e)
+        return lam, grad, work_dict(w)
+
     def model_eval(self, model, what, t, y, w=None):
         """what: 0 rate, 1 jacobian, 2 parameter_vjp (accumulated from zero)."""
         t = np.ascontiguousarray(t, np.float64)

@@ -200,6 +200,56 @@ int ref_adjoint(const cko_model_desc* d, const double* states, const double* tim
   }
 }
 
+// integrate_forward_euler (integrate.cpp:371-407).
+int ref_fe_forward(const cko_model_desc* d, const double* y0, const double* times, int nb, int nt, int n_chunk,
+                   double* states_out, cko_work* work, cko_error* err) {
+  try {
+    auto m = build(d);
+    Array2d Y0(nb, m->state_size());
+    std::memcpy(Y0.data(), y0, sizeof(double) * Y0.size());
+    Trajectory tr = integrate_forward_euler(*m, Y0, grid_of(times, nb, nt), n_chunk);
+    std::memcpy(states_out, tr.states.data(), sizeof(double) * tr.states.size());
+    put_work(work, tr.work);
+    fill(err, CKO_OK, "");
+    return 0;
+  } catch (...) {
+    return map_exception(err);
+  }
+}
+
+// adjoint_backward(..., Scheme::forward_euler, ...) (adjoint.cpp:157-188, 263-297).
+int ref_fe_adjoint(const cko_model_desc* d, const double* states, const double* times, int nb, int nt, int n_chunk,
+                   int loss_kind, const double* dL, double* loss_out, double* grad_out, cko_work* bwd,
+                   cko_error* err) {
+  try {
+    auto m = build(d);
+    Trajectory tr;
+    tr.grid = grid_of(times, nb, nt);
+    tr.n_batch = nb;
+    tr.n_size = m->state_size();
+    tr.states = Array2d(nt + 1, nb * tr.n_size);
+    std::memcpy(tr.states.data(), states, sizeof(double) * tr.states.size());
+    LossSpec loss = loss_frobenius();
+    if (loss_kind == CKO_LOSS_USER) {
+      const double* g = dL;
+      loss.value = [](const Trajectory&) { return std::nan(""); };
+      loss.state_gradient = [g](const Trajectory&, Array2d& out) {
+        std::memcpy(out.data(), g, sizeof(double) * out.size());
+      };
+    }
+    WorkCounters w;
+    auto [L, grad] = adjoint_backward(*m, tr, n_chunk, loss, Scheme::forward_euler, SolverChoice{},
+                                      JacobianStrategy::analytic, &w);
+    if (loss_out) *loss_out = L;
+    std::memcpy(grad_out, grad.data(), sizeof(double) * grad.size());
+    put_work(bwd, w);
+    fill(err, CKO_OK, "");
+    return 0;
+  } catch (...) {
+    return map_exception(err);
+  }
+}
+
 // gradient_adjoint (adjoint.cpp:299-313) with timings of both phases.
 int ref_gradient_adjoint(const cko_model_desc* d, const double* y0, const double* times, int nb,
                          int nt, int n_chunk, const cko_newton_settings* st,
@@ -371,6 +421,89 @@ int ref_model_eval(const cko_model_desc* d, int what, const double* t, const dou
       std::span<double> g(out, m->params().size());
       parameter_vjp(*m, T, Y, W, g);
     }
+    fill(err, CKO_OK, "");
+    return 0;
+  } catch (...) {
+    return map_exception(err);
+  }
+}
+
+// Public single-chunk ops of the reference (integrate.hpp:53-67, adjoint.hpp:36-56).
+// op 0 chunk_residual -> out (c, nb, n); op 1 chunk_jacobian -> out diag (c, nb, n, n)
+// and out2 offdiag (c-1, nb, n, n); op 2 newton_solve_chunk -> dy in/out, iters.
+int ref_chunk_op(const cko_model_desc* d, int op, const double* y_start, double* dy,
+                 const double* t_chunk, const double* dt_chunk, int c, int nb,
+                 const cko_newton_settings* st, const cko_solver_choice* sv, double* out,
+                 double* out2, int* iters, cko_work* work, cko_error* err) {
+  try {
+    auto m = build(d);
+    const int n = m->state_size();
+    Array2d ys(nb, n), T(c, nb), DT(c, nb);
+    std::memcpy(ys.data(), y_start, sizeof(double) * ys.size());
+    std::memcpy(T.data(), t_chunk, sizeof(double) * T.size());
+    std::memcpy(DT.data(), dt_chunk, sizeof(double) * DT.size());
+    BatchedChunkVector D(c, nb, n);
+    std::memcpy(D.data(), dy, sizeof(double) * D.size());
+    if (op == 0) {
+      BatchedChunkVector o(c, nb, n);
+      chunk_residual(*m, ys, D, T, DT, o);
+      std::memcpy(out, o.data(), sizeof(double) * o.size());
+    } else if (op == 1) {
+      BlockBidiagonalSystem sys(c, nb, n);
+      chunk_jacobian(*m, ys, D, T, DT, JacobianStrategy::analytic, sys);
+      std::memcpy(out, sys.diag.data(), sizeof(double) * sys.diag.size());
+      if (out2 && c > 1) std::memcpy(out2, sys.offdiag.data(), sizeof(double) * sys.offdiag.size());
+    } else {
+      WorkCounters w;
+      NewtonSettings ns{st->tol_a, st->tol_r, st->max_iter};
+      const int it = newton_solve_chunk(*m, ys, D, T, DT, ns, solver_of(sv), JacobianStrategy::analytic, &w, 1);
+      std::memcpy(dy, D.data(), sizeof(double) * D.size());
+      if (iters) *iters = it;
+      put_work(work, w);
+    }
+    fill(err, CKO_OK, "");
+    return 0;
+  } catch (...) {
+    return map_exception(err);
+  }
+}
+
+// adjoint_chunk_solve over a host trajectory (op 0) or adjoint_step_sequential
+// (op 1: states rows [y_prev; y_i], times rows [t_prev; t_i], dL row 1 = dL_i).
+int ref_adjoint_chunk(const cko_model_desc* d, int op, const double* states, const double* times,
+                      int nb, int nt, int step_hi, int chunk_len, const double* dL,
+                      const cko_solver_choice* sv, double* lambda, double* grad, cko_work* work,
+                      cko_error* err) {
+  try {
+    auto m = build(d);
+    const int n = m->state_size();
+    AdjointState state;
+    state.lambda = Array2d(nb, n);
+    std::memcpy(state.lambda.data(), lambda, sizeof(double) * state.lambda.size());
+    state.grad.assign(grad, grad + m->params().size());
+    if (op == 0) {
+      Trajectory tr;
+      tr.grid = grid_of(times, nb, nt);
+      tr.n_batch = nb;
+      tr.n_size = n;
+      tr.states = Array2d(nt + 1, nb * n);
+      std::memcpy(tr.states.data(), states, sizeof(double) * tr.states.size());
+      Array2d G(nt + 1, nb * n);
+      std::memcpy(G.data(), dL, sizeof(double) * G.size());
+      WorkCounters w;
+      adjoint_chunk_solve(*m, tr, step_hi, chunk_len, G, state, solver_of(sv), JacobianStrategy::analytic, &w);
+      put_work(work, w);
+    } else {
+      Array2d yi(nb, n), yp(nb, n), g(nb, n);
+      std::memcpy(yp.data(), states, sizeof(double) * yp.size());
+      std::memcpy(yi.data(), states + size_t(nb) * n, sizeof(double) * yi.size());
+      std::memcpy(g.data(), dL + size_t(nb) * n, sizeof(double) * g.size());
+      adjoint_step_sequential(*m, yi, yp, std::span<const double>(times + nb, nb),
+                              std::span<const double>(times, nb), g, state, solver_of(sv),
+                              JacobianStrategy::analytic);
+    }
+    std::memcpy(lambda, state.lambda.data(), sizeof(double) * state.lambda.size());
+    std::memcpy(grad, state.grad.data(), sizeof(double) * state.grad.size());
     fill(err, CKO_OK, "");
     return 0;
   } catch (...) {

@@ -67,6 +67,14 @@ def lib() -> C.CDLL:
         "cko_ctx_kernel_generation_used": ([vp], C.c_int),
         "cko_newton_solve_chunk": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, P(N), P(S), C.c_int, P(C.c_int), P(W),
                                     P(E)], C.c_int),
+        "cko_chunk_residual": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, dp, P(E)], C.c_int),
+        "cko_chunk_jacobian": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, dp, dp, P(E)], C.c_int),
+        "cko_adjoint_chunk_solve": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, dp, P(S), dp, dp, P(W),
+                                     P(E)], C.c_int),
+        "cko_adjoint_step_sequential": ([vp, vp, dp, dp, dp, dp, dp, C.c_int, P(S), dp, dp, P(E)], C.c_int),
+        "cko_fe_forward": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, dp, P(W), P(E)], C.c_int),
+        "cko_fe_adjoint_host": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, dp, P(W), P(E)],
+                                C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -86,5 +94,6 @@ EXPORTS = [
     "cko_gradient_adjoint", "cko_traj_states", "cko_traj_destroy", "cko_block_bidiag_solve",
     "cko_newton_solve_chunk", "cko_ctx_enable_timing", "cko_ctx_last_kernel_ms", "cko_ctx_last_launches",
     "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open", "cko_ctx_set_kernel_generation",
-    "cko_ctx_kernel_generation_used",
+    "cko_ctx_kernel_generation_used", "cko_chunk_residual", "cko_chunk_jacobian", "cko_adjoint_chunk_solve",
+    "cko_adjoint_step_sequential", "cko_fe_forward", "cko_fe_adjoint_host",
 ]

@@ -260,9 +260,34 @@ def integrate_backward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int,
     return Trajectory(states, grid, nb, n, WorkCounters.from_c(w))
 
 
+class Scheme:
+    """adjoint.hpp:12: the discrete adjoint follows the scheme that produced the trajectory."""
+    backward_euler = "backward_euler"
+    forward_euler = "forward_euler"
+
+
+def integrate_forward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int = 1,
+                            ctx: Context | None = None) -> Trajectory:
+    """integrate.hpp:91-96: explicit, strictly step-sequential (results independent of n_chunk)."""
+    y0 = _f64(y0)
+    if y0.ndim != 2 or y0.shape[1] != model.state_size:
+        raise ShapeMismatch("integrate: y0 width != state size")
+    if y0.shape[0] != grid.n_batch:
+        raise ShapeMismatch("integrate: y0 rows != grid batch width")
+    if n_chunk < 1:
+        raise ShapeMismatch("integrate: n_chunk must be >= 1")
+    ctx = ctx or default_context()
+    nb, nt, n = grid.n_batch, grid.n_time, model.state_size
+    states = np.zeros((nt + 1, nb * n))
+    w, e = abi.CkoWork(), abi.CkoError()
+    raise_for(lib().cko_fe_forward(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
+                                   dptr(states), C.byref(w), C.byref(e)), e)
+    return Trajectory(states, grid, nb, n, WorkCounters.from_c(w))
+
+
 def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpec | None = None,
                      solver: SolverChoice | None = None, work: WorkCounters | None = None,
-                     ctx: Context | None = None):
+                     ctx: Context | None = None, scheme: str = Scheme.backward_euler):
     """Returns (loss, gradient) like adjoint.hpp:63-66; `work` (if given) receives the backward counters."""
     loss = loss or loss_frobenius()
     solver = solver or SolverChoice()
@@ -284,9 +309,14 @@ def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpe
         dL = _f64(loss.state_gradient(traj))
         if dL.shape != traj.states.shape:
             raise ShapeMismatch("loss gradient: output must be shaped like the trajectory states")
-    rc = lib().cko_be_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
-                                   traj.n_batch, traj.n_time, int(n_chunk), C.byref(sv), kind, dptr(dL),
-                                   C.byref(L), dptr(grad), C.byref(w), C.byref(e))
+    if scheme == Scheme.forward_euler:
+        rc = lib().cko_fe_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
+                                       traj.n_batch, traj.n_time, int(n_chunk), kind, dptr(dL), C.byref(L),
+                                       dptr(grad), C.byref(w), C.byref(e))
+    else:
+        rc = lib().cko_be_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
+                                       traj.n_batch, traj.n_time, int(n_chunk), C.byref(sv), kind, dptr(dL),
+                                       C.byref(L), dptr(grad), C.byref(w), C.byref(e))
     raise_for(rc, e)
     if work is not None:
         work += WorkCounters.from_c(w)
@@ -296,11 +326,16 @@ def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpe
 
 def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossSpec | None = None,
                      solver: SolverChoice | None = None, settings: NewtonSettings | None = None,
-                     ctx: Context | None = None) -> GradientResult:
+                     ctx: Context | None = None, scheme: str = Scheme.backward_euler) -> GradientResult:
     """adjoint.cpp:299-313; the Frobenius loss runs fully on the device."""
     loss = loss or loss_frobenius()
     settings = settings or NewtonSettings()
     solver = solver or SolverChoice()
+    if scheme == Scheme.forward_euler:
+        tr = integrate_forward_euler(model, y0, grid, n_chunk, ctx)
+        bw = WorkCounters()
+        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx, scheme=scheme)
+        return GradientResult(L, g, tr, bw)
     if not loss.frobenius:
         tr = integrate_backward_euler(model, y0, grid, n_chunk, settings, solver, ctx)
         bw = WorkCounters()
@@ -346,6 +381,123 @@ def newton_solve_chunk(model: Model, y_start, dy, t_chunk, dt_chunk, settings: N
     if work is not None:
         work += WorkCounters.from_c(w)
     return int(it.value)
+
+
+def _chunk_args(model: Model, y_start, dy, t_chunk, dt_chunk):
+    """check_chunk_args (integrate.cpp:12-21)."""
+    y_start, dy = _f64(y_start), _f64(dy)
+    t_chunk, dt_chunk = _f64(t_chunk), _f64(dt_chunk)
+    n = model.state_size
+    if y_start.ndim != 2 or y_start.shape[1] != n:
+        raise ShapeMismatch("chunk op: y_start width != state size")
+    if dy.ndim != 3 or dy.shape[2] != n:
+        raise ShapeMismatch("chunk op: dy width != state size")
+    if y_start.shape[0] != dy.shape[1]:
+        raise ShapeMismatch("chunk op: y_start rows != batch width")
+    if t_chunk.shape != dy.shape[:2]:
+        raise ShapeMismatch("chunk op: t_chunk must be (chunk_len, n_batch)")
+    if dt_chunk.shape != dy.shape[:2]:
+        raise ShapeMismatch("chunk op: dt_chunk must be (chunk_len, n_batch)")
+    return y_start, dy, t_chunk, dt_chunk
+
+
+def chunk_residual(model: Model, y_start, dy, t_chunk, dt_chunk, ctx: Context | None = None) -> np.ndarray:
+    """integrate.hpp:53-55: out(j) = dy(j) - dy(j-1) - h(y_start + dy(j), t(j)) dt(j), shape (c, nb, n)."""
+    y_start, dy, t_chunk, dt_chunk = _chunk_args(model, y_start, dy, t_chunk, dt_chunk)
+    ctx = ctx or default_context()
+    c, nb, n = dy.shape
+    out = np.empty_like(dy)
+    e = abi.CkoError()
+    raise_for(lib().cko_chunk_residual(ctx.h, ctx.model(model), dptr(y_start), dptr(dy), dptr(t_chunk),
+                                       dptr(dt_chunk), c, nb, dptr(out), C.byref(e)), e)
+    return out
+
+
+def chunk_jacobian(model: Model, y_start, dy, t_chunk, dt_chunk, ctx: Context | None = None) -> "BlockBidiagonalSystem":
+    """integrate.hpp:57-61 (analytic Jacobian): diag I - J dt, offdiag -I."""
+    y_start, dy, t_chunk, dt_chunk = _chunk_args(model, y_start, dy, t_chunk, dt_chunk)
+    ctx = ctx or default_context()
+    c, nb, n = dy.shape
+    sys = BlockBidiagonalSystem.zeros(c, nb, n)
+    e = abi.CkoError()
+    raise_for(lib().cko_chunk_jacobian(ctx.h, ctx.model(model), dptr(y_start), dptr(dy), dptr(t_chunk),
+                                       dptr(dt_chunk), c, nb, dptr(sys.diag), dptr(sys.offdiag) if c > 1 else None,
+                                       C.byref(e)), e)
+    return sys
+
+
+@dataclass
+class AdjointState:
+    """adjoint.hpp:26-31: lambda (n_batch, n_size) and the gradient accumulator (n_params)."""
+
+    lam: np.ndarray
+    grad: np.ndarray
+
+    @classmethod
+    def zeros(cls, model: Model, n_batch: int) -> "AdjointState":
+        return cls(np.zeros((n_batch, model.state_size)), np.zeros(model.params.size))
+
+
+def _check_state(model: Model, state: AdjointState, nb: int):
+    """check_adjoint_state (adjoint.cpp:129-134)."""
+    if state.lam.shape != (nb, model.state_size):
+        raise ShapeMismatch("adjoint: lambda must be (n_batch, n_size)")
+    if state.grad.shape != (model.params.size,):
+        raise ShapeMismatch("adjoint: gradient accumulator length != parameter count")
+
+
+def adjoint_chunk_solve(model: Model, traj: Trajectory, step_hi: int, chunk_len: int, dL_dy, state: AdjointState,
+                        solver: SolverChoice | None = None, work: WorkCounters | None = None,
+                        ctx: Context | None = None) -> None:
+    """adjoint.hpp:49-56: reverse steps step_hi - chunk_len + 1 .. step_hi in one coupled solve; updates
+    state.lam and accumulates into state.grad."""
+    solver = solver or SolverChoice()
+    if traj.n_size != model.state_size:
+        raise ShapeMismatch("adjoint chunk: trajectory width != model size")
+    if not (chunk_len >= 1 and step_hi >= chunk_len and step_hi <= traj.n_time):
+        raise ShapeMismatch("adjoint chunk: step range out of bounds")
+    dL = _f64(dL_dy)
+    if dL.shape != traj.states.shape:
+        raise ShapeMismatch("adjoint chunk: dL_dy must be shaped like the trajectory states")
+    _check_state(model, state, traj.n_batch)
+    ctx = ctx or default_context()
+    lam, grad = _f64(state.lam).copy(), _f64(state.grad).copy()
+    w, e = abi.CkoWork(), abi.CkoError()
+    sv = solver.c()
+    raise_for(lib().cko_adjoint_chunk_solve(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
+                                            traj.n_batch, traj.n_time, int(step_hi), int(chunk_len), dptr(dL),
+                                            C.byref(sv), dptr(lam), dptr(grad), C.byref(w), C.byref(e)), e)
+    state.lam[...] = lam
+    state.grad[...] = grad
+    if work is not None:
+        work += WorkCounters.from_c(w)
+
+
+def adjoint_step_sequential(model: Model, y_i, y_prev, t_i, t_prev, dL_dy_i, state: AdjointState,
+                            solver: SolverChoice | None = None, ctx: Context | None = None) -> None:
+    """adjoint.hpp:36-47: one reverse backward-Euler step, state updated in place."""
+    solver = solver or SolverChoice()
+    y_i, y_prev, dl = _f64(y_i), _f64(y_prev), _f64(dL_dy_i)
+    t_i, t_prev = _f64(t_i), _f64(t_prev)
+    nb, n = y_i.shape
+    if n != model.state_size:
+        raise ShapeMismatch("adjoint step: state width != model size")
+    if y_prev.shape != (nb, n):
+        raise ShapeMismatch("adjoint step: y_prev shape")
+    if t_i.shape != (nb,) or t_prev.shape != (nb,):
+        raise ShapeMismatch("adjoint step: time spans")
+    if dl.shape != (nb, n):
+        raise ShapeMismatch("adjoint step: loss jump shape")
+    _check_state(model, state, nb)
+    ctx = ctx or default_context()
+    lam, grad = _f64(state.lam).copy(), _f64(state.grad).copy()
+    e = abi.CkoError()
+    sv = solver.c()
+    raise_for(lib().cko_adjoint_step_sequential(ctx.h, ctx.model(model), dptr(y_i), dptr(y_prev), dptr(t_i),
+                                                dptr(t_prev), dptr(dl), nb, C.byref(sv), dptr(lam), dptr(grad),
+                                                C.byref(e)), e)
+    state.lam[...] = lam
+    state.grad[...] = grad
 
 
 # ---------------------------------------------------------------------------

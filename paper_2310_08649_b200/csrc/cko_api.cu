@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -471,7 +472,7 @@ constexpr int kThreads = 256;
 // Core forward on device buffers (states row 0 must hold y0).
 cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
                         int nc, const cko_newton_settings* st, const cko_solver_choice* sv, const double* d_dy,
-                        cko_work* work, int* iters_out, cko_error* err) {
+                        cko_work* work, int* iters_out, cko_error* err, const double* d_dts = nullptr) {
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
   if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
   if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
@@ -481,10 +482,10 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   const int n = m->dm.n;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const bool nodep = !pcr && c->kernel_gen >= 2 && node_fast_path(m->dm);
-  const bool v2 = !nodep && !pcr && c->kernel_gen >= 2 &&
-                  launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
-  const bool p2 = pcr && c->kernel_gen >= 2 && launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const int gen = d_dts ? 1 : c->kernel_gen;  // explicit step sizes: generic kernels (single-chunk op)
+  const bool nodep = !pcr && gen >= 2 && node_fast_path(m->dm);
+  const bool v2 = !nodep && !pcr && gen >= 2 && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const bool p2 = pcr && gen >= 2 && launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   int G;
   Slab slab;
   if (v2 || p2) {
@@ -516,6 +517,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.states = d_states;
   a.times = d_times;
   a.dy_init = d_dy;
+  a.dts = d_dts;
   a.nb = nb;
   a.nt = nt;
   a.nc = nc;
@@ -653,7 +655,8 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
 // Core adjoint on device buffers.
 cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times, int nb,
                         int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* d_dL,
-                        double* loss_out, double* grad_out, cko_work* bwd, cko_error* err) {
+                        double* loss_out, double* grad_out, cko_work* bwd, cko_error* err,
+                        bool keep_lambda = false) {
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
   if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
   if (sv->kind == CKO_SOLVER_HYBRID && sv->n_switch < 0)
@@ -663,10 +666,10 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   const int n = m->dm.n, np = m->dm.np;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const bool nodep = !pcr && c->kernel_gen >= 2 && node_fast_path(m->dm);
-  const bool v2 = !nodep && !pcr && c->kernel_gen >= 2 &&
-                  launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
-  const bool p2 = pcr && c->kernel_gen >= 2 && launch_adjoint_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const int gen = keep_lambda ? 1 : c->kernel_gen;  // a carried-in lambda: generic kernels (single-chunk op)
+  const bool nodep = !pcr && gen >= 2 && node_fast_path(m->dm);
+  const bool v2 = !nodep && !pcr && gen >= 2 && launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  const bool p2 = pcr && gen >= 2 && launch_adjoint_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const int G = (v2 || p2) ? (nb < c->sms ? nb : c->sms) : (nb < 2 * c->sms ? nb : 2 * c->sms);
   Slab slab{};
   if (nodep) {
@@ -715,6 +718,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.n_switch = sv->n_switch;
   a.slab = slab;
   a.lambda = c->lambda.as<double>();
+  a.keep_lambda = keep_lambda ? 1 : 0;
   a.wq = c->wq.as<double>();
   a.sing_key = c->key.as<unsigned long long>();
   a.grid = G;
@@ -790,9 +794,152 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   return ok(err);
 }
 
+// ---- forward Euler scheme (integrate.cpp:371-407, adjoint.cpp:157-188) ----------------------------
+cko_status fe_forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
+                           int nc, cko_work* work, cko_error* err) {
+  if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
+  if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
+  if (cko_status s = check_lanes(m, nb, err)) return s;
+  CUDA_TRY(c->scratch.ensure(sizeof(double) * (size_t)nb * m->dm.n));
+  CUDA_TRY(c->info.ensure(sizeof(int) * 4));
+  CUDA_TRY(c->pin.ensure(64));
+  CUDA_TRY(cudaMemsetAsync(c->info.p, 0x7f, sizeof(int), c->stream));
+  c->mark(0);
+  CUDA_TRY(launch_fe_forward(m->dm, d_states, d_times, nb, nt, c->scratch.as<double>(), c->info.as<int>(), c->stream));
+  c->mark(1);
+  CUDA_TRY(cudaMemcpyAsync(c->pin.p, c->info.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->last_launches = 1;
+  c->last_gen = 1;
+  c->last_ms[1] = c->last_ms[2] = c->last_ms[3] = 0.0;
+  c->collect(0, 1);
+  const int bad = *c->pin.as<int>(0);
+  if (bad != 0x7f7f7f7f)
+    return fail(err, CKO_NON_FINITE, "forward Euler produced a non-finite state at step %d", bad);
+  if (work) {
+    std::memset(work, 0, sizeof(*work));
+    work->rate_evals = nt;  // one batched rate call per step
+  }
+  return ok(err);
+}
+
+cko_status fe_adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times, int nb,
+                           int nt, int nc, int loss_kind, const double* d_dL, double* loss_out, double* grad_out,
+                           cko_work* bwd, cko_error* err) {
+  if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
+  if (loss_kind == CKO_LOSS_USER && !d_dL) return fail(err, CKO_ERROR, "user loss needs dL");
+  if (cko_status s = check_lanes(m, nb, err)) return s;
+  const int n = m->dm.n, np = m->dm.np;
+  const size_t row = (size_t)nb * n;
+  CUDA_TRY(c->lambda.ensure(sizeof(double) * row));
+  CUDA_TRY(c->wq.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->slab.ensure(sizeof(double) * (row * n + row)));
+  CUDA_TRY(c->key.ensure(sizeof(unsigned long long)));
+  CUDA_TRY(c->loss.ensure(sizeof(double)));
+  CUDA_TRY(c->scratch.ensure(sizeof(double) * 1040));
+  CUDA_TRY(c->status.ensure(2 * sizeof(unsigned)));
+  CUDA_TRY(c->vjp.ensure(sizeof(double) * vjp_scratch_doubles(m->dm, nb, nt)));
+  CUDA_TRY(c->grad.ensure(sizeof(double) * (np + 1)));
+  if (c->grp.world > 1 && np + 1 > c->grp.red_cap)
+    return fail(err, CKO_COMM, "parameter count %d exceeds the group reduce buffer (%d)", np, c->grp.red_cap);
+  CUDA_TRY(cudaMemsetAsync(c->status.p, 0, 2 * sizeof(unsigned), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+  c->last_launches = 3;
+  c->last_gen = 1;
+  c->mark(6);
+  if (loss_kind == CKO_LOSS_FROBENIUS) {
+    CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
+                         c->gs.as<GridSync>(), c->status.as<unsigned>(), c->stream));
+    c->last_launches += 2;
+  }
+  c->mark(7);
+  c->mark(2);
+  double* Jb = c->slab.as<double>();
+  CUDA_TRY(launch_fe_adjoint(m->dm, d_states, d_times, loss_kind == CKO_LOSS_USER ? d_dL : nullptr,
+                             loss_kind == CKO_LOSS_USER ? nullptr : c->loss.as<double>(), nb, nt, c->lambda.as<double>(),
+                             Jb, Jb + row * n, c->wq.as<double>(), c->status.as<unsigned>() + 1, c->stream));
+  c->mark(3);
+  c->mark(4);
+  // the quadrature of step m sits at the step START (y_{m-1}, t_{m-1}): the VJP kernels read row-shifted views
+  const double* st_prev = reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(d_states) - sizeof(double) * row);
+  const double* t_prev = reinterpret_cast<const double*>(reinterpret_cast<uintptr_t>(d_times) - sizeof(double) * nb);
+  CUDA_TRY(launch_vjp(m->dm, st_prev, t_prev, c->wq.as<double>(), nb, nt, c->vjp.as<double>(), c->grad.as<double>(),
+                      c->stream));
+  if (c->grp.world > 1) {
+    CUDA_TRY(launch_group_sum(c->grp, c->gs.as<GridSync>(), c->grad.as<double>(), np, c->status.as<unsigned>(),
+                              c->stream));
+    c->last_launches += 1;
+  }
+  c->mark(5);
+  CUDA_TRY(c->pin.ensure(32 + sizeof(double) * (size_t)(np + 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned>(0), c->status.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                           c->stream));
+  if (loss_kind == CKO_LOSS_FROBENIUS)
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(16), c->loss.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->pin.as<double>(32), c->grad.p, sizeof(double) * np, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const unsigned gstatus = c->pin.as<unsigned>(0)[0], jbad = c->pin.as<unsigned>(0)[1];
+  const double L = loss_kind == CKO_LOSS_FROBENIUS ? *c->pin.as<double>(16) : NAN;
+  std::memcpy(grad_out, c->pin.as<double>(32), sizeof(double) * np);
+  c->last_ms[0] = 0.0;
+  c->collect(1, 3);
+  if (gstatus) return fail(err, CKO_COMM, "group reduction timed out (peer stalled)");
+  if (jbad) return fail(err, CKO_NON_FINITE, "Jacobian of the model is not finite");
+  for (int j = 0; j < np; ++j)
+    if (!std::isfinite(grad_out[j])) return fail(err, CKO_NON_FINITE, "parameter product of the model is not finite");
+  if (loss_out) *loss_out = L;
+  if (bwd) {
+    std::memset(bwd, 0, sizeof(*bwd));
+    for (int step_hi = nt; step_hi >= 1; step_hi -= (nc < step_hi ? nc : step_hi)) bwd->jacobian_evals += 1;
+  }
+  return ok(err);
+}
+
 }  // namespace
 
 extern "C" {
+
+cko_status cko_fe_forward(cko_ctx* c, const cko_model* m, const double* y0, const double* times, int nb, int nt,
+                          int nc, double* states_out, cko_work* work, cko_error* err) {
+  if (!c || !m || !y0 || !times || !states_out) return fail(err, CKO_ERROR, "null argument");
+  if (cko_status s = check_grid_shape(nt, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
+  double* d_states = c->h_states.as<double>();
+  double* d_times = c->h_times.as<double>();
+  CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
+  if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
+  if (cko_status s = fe_forward_core(c, m, d_states, d_times, nb, nt, nc, work, err)) return s;
+  CUDA_TRY(cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return ok(err);
+}
+
+cko_status cko_fe_adjoint_host(cko_ctx* c, const cko_model* m, const double* states, const double* times, int nb,
+                               int nt, int nc, int loss_kind, const double* dL_host, double* loss_out,
+                               double* grad_out, cko_work* bwd, cko_error* err) {
+  if (!c || !m || !states || !times || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (cko_status s = check_grid_shape(nt, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (nt + 1)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
+  CUDA_TRY(cudaMemcpyAsync(c->h_states.p, states, sizeof(double) * row * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice,
+                           c->stream));
+  const double* d_dL = nullptr;
+  if (loss_kind == CKO_LOSS_USER) {
+    if (!dL_host) return fail(err, CKO_ERROR, "user loss needs dL");
+    CUDA_TRY(c->h_dL.ensure(sizeof(double) * row * (nt + 1)));
+    CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dL_host, sizeof(double) * row * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+    d_dL = c->h_dL.as<double>();
+  }
+  return fe_adjoint_core(c, m, c->h_states.as<double>(), c->h_times.as<double>(), nb, nt, nc, loss_kind, d_dL,
+                         loss_out, grad_out, bwd, err);
+}
 
 cko_status cko_be_forward_device(cko_ctx* c, const cko_model* m, const double* d_y0, const double* d_times, int nb,
                                  int nt, int nc, const cko_newton_settings* st, const cko_solver_choice* sv,
@@ -1020,41 +1167,151 @@ cko_status cko_newton_solve_chunk(cko_ctx* c, const cko_model* m, const double* 
   if (!c || !m || !y_start || !dy || !t_chunk || !dt_chunk || !st || !sv) return fail(err, CKO_ERROR, "null argument");
   if (cc < 1 || nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "chunk op: empty chunk");
   CUDA_TRY(cudaSetDevice(c->device));
-  // A one-chunk integration over a synthetic grid reproducing t_chunk/dt_chunk:
-  // times row 0 = t_0 - dt_0, row k+1 = t_chunk(k). dt is recomputed on the
-  // device as t(k) - t(k-1), so feed the exact differences through
-  // consecutive rows: t_prev(k) = t(k) - dt(k) must equal t(k-1).
+  // One chunk through the generic forward kernel with explicit step sizes: rate times are t_chunk (rows
+  // 1..c of a (c+1)-row grid, row 0 unused), dt(k) = dt_chunk(k) exactly as newton_chunk reads them
+  // (integrate.cpp:64-95, 118-135) — dt_chunk need not equal the differences of t_chunk.
   const int n = m->dm.n;
-  std::vector<double> times((size_t)(cc + 1) * nb);
-  for (int b = 0; b < nb; ++b) {
-    times[b] = t_chunk[b] - dt_chunk[b];
-    for (int k = 0; k < cc; ++k) times[(size_t)(k + 1) * nb + b] = t_chunk[(size_t)k * nb + b];
-  }
-  for (int k = 1; k < cc; ++k)
-    for (int b = 0; b < nb; ++b)
-      if (t_chunk[(size_t)k * nb + b] - t_chunk[(size_t)(k - 1) * nb + b] != dt_chunk[(size_t)k * nb + b])
-        return fail(err, CKO_STRATEGY_UNAVAILABLE,
-                    "newton_solve_chunk: dt_chunk must equal consecutive t_chunk differences on the device path");
-  const size_t row = (size_t)nb * n;
+  const size_t row = (size_t)nb * n, trow = (size_t)nb;
   CUDA_TRY(c->h_states.ensure(sizeof(double) * row * (cc + 1)));
-  CUDA_TRY(c->h_times.ensure(sizeof(double) * times.size()));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * trow * (cc + 1 + cc)));
   CUDA_TRY(c->h_dL.ensure(sizeof(double) * row * cc));
   double* d_states = c->h_states.as<double>();
-  CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times.data(), sizeof(double) * times.size(), cudaMemcpyHostToDevice, c->stream));
+  double* d_times = c->h_times.as<double>();
+  double* d_dts = d_times + trow * (cc + 1);
+  CUDA_TRY(cudaMemcpyAsync(d_times + trow, t_chunk, sizeof(double) * trow * cc, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_times, t_chunk, sizeof(double) * trow, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_dts, dt_chunk, sizeof(double) * trow * cc, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(d_states, y_start, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dy, sizeof(double) * row * cc, cudaMemcpyHostToDevice, c->stream));
-  cko_newton_settings s2 = *st;
-  cko_status s = forward_core(c, m, d_states, c->h_times.as<double>(), nb, cc, cc, &s2, sv, c->h_dL.as<double>(),
-                              work, iterations, err);
+  cko_status s = forward_core(c, m, d_states, d_times, nb, cc, cc, st, sv, c->h_dL.as<double>(), work, iterations,
+                              err, d_dts);
   if (s != CKO_OK) {
     if (s == CKO_NEWTON_DIVERGENCE && err) err->chunk_start_step = chunk_start_step;
     return s;
   }
   std::vector<double> out(row * (cc + 1));
-  CUDA_TRY(cudaMemcpy(out.data(), d_states, sizeof(double) * out.size(), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpyAsync(out.data(), d_states, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
   for (int k = 0; k < cc; ++k)
     for (size_t i = 0; i < row; ++i) dy[(size_t)k * row + i] = out[(size_t)(k + 1) * row + i] - y_start[i];
   return ok(err);
+}
+
+// chunk_residual / chunk_jacobian (integrate.cpp:269-297) on the device.
+static cko_status chunk_op(cko_ctx* c, const cko_model* m, int op, const double* y_start, const double* dy,
+                           const double* t_chunk, const double* dt_chunk, int cc, int nb, double* out,
+                           double* offdiag_out, cko_error* err) {
+  if (!c || !m || !y_start || !dy || !t_chunk || !dt_chunk || !out) return fail(err, CKO_ERROR, "null argument");
+  if (cc < 1 || nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "chunk op: empty chunk");
+  if (cko_status s = check_lanes(m, nb, err)) return s;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int n = m->dm.n;
+  const size_t P = (size_t)cc * nb, nout = op == 0 ? P * n : P * n * n;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * (2 * P * n + (size_t)nb * n)));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * 2 * P));
+  CUDA_TRY(c->h_diag.ensure(sizeof(double) * nout));
+  CUDA_TRY(c->status.ensure(sizeof(unsigned)));
+  double* d_ys = c->h_states.as<double>();
+  double* d_dy = d_ys + (size_t)nb * n;
+  double* d_yy = d_dy + P * n;
+  double* d_t = c->h_times.as<double>();
+  double* d_dt = d_t + P;
+  CUDA_TRY(cudaMemcpyAsync(d_ys, y_start, sizeof(double) * nb * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_dy, dy, sizeof(double) * P * n, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_t, t_chunk, sizeof(double) * P, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_dt, dt_chunk, sizeof(double) * P, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->status.p, 0, sizeof(unsigned), c->stream));
+  CUDA_TRY(launch_chunk_op(m->dm, op, d_ys, d_dy, d_t, d_dt, cc, nb, d_yy, c->h_diag.as<double>(),
+                           c->status.as<unsigned>(), c->stream));
+  unsigned flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(out, c->h_diag.p, sizeof(double) * nout, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&flag, c->status.p, sizeof flag, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->last_launches = 1;
+  c->last_gen = 1;
+  if (flag)
+    return fail(err, CKO_NON_FINITE, op == 0 ? "chunk_residual: model rate returned a non-finite value"
+                                             : "Jacobian of the model is not finite");
+  if (op == 1 && offdiag_out && cc > 1) {  // the -I couplings (fill_unit_offdiag, integrate.cpp:140-147)
+    const size_t no = (size_t)(cc - 1) * nb * n * n;
+    std::memset(offdiag_out, 0, sizeof(double) * no);
+    for (size_t blk = 0; blk < (size_t)(cc - 1) * nb; ++blk)
+      for (int i = 0; i < n; ++i) offdiag_out[blk * n * n + (size_t)i * n + i] = -1.0;
+  }
+  return ok(err);
+}
+
+cko_status cko_chunk_residual(cko_ctx* c, const cko_model* m, const double* y_start, const double* dy,
+                              const double* t_chunk, const double* dt_chunk, int cc, int nb, double* out,
+                              cko_error* err) {
+  return chunk_op(c, m, 0, y_start, dy, t_chunk, dt_chunk, cc, nb, out, nullptr, err);
+}
+
+cko_status cko_chunk_jacobian(cko_ctx* c, const cko_model* m, const double* y_start, const double* dy,
+                              const double* t_chunk, const double* dt_chunk, int cc, int nb, double* diag_out,
+                              double* offdiag_out, cko_error* err) {
+  return chunk_op(c, m, 1, y_start, dy, t_chunk, dt_chunk, cc, nb, diag_out, offdiag_out, err);
+}
+
+// One reversed chunk over host rows lo = step_hi - chunk_len .. step_hi of a trajectory: the rows are
+// staged as a (chunk_len + 1)-row mini trajectory and reversed as its only chunk, lambda carried in and
+// out, the chunk's parameter product added to grad (be_chunk_core, adjoint.cpp:49-127).
+static cko_status chunk_reverse(cko_ctx* c, const cko_model* m, const double* states_rows, const double* times_rows,
+                                const double* dL_rows, int nb, int chunk_len, const cko_solver_choice* sv,
+                                double* lambda, double* grad, cko_work* work, cko_error* err) {
+  const int n = m->dm.n, np = m->dm.np;
+  const size_t row = (size_t)nb * n, rows = (size_t)chunk_len + 1;
+  CUDA_TRY(c->h_states.ensure(sizeof(double) * row * rows));
+  CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * rows));
+  CUDA_TRY(c->h_dL.ensure(sizeof(double) * row * rows));
+  CUDA_TRY(c->lambda.ensure(sizeof(double) * row));
+  CUDA_TRY(cudaMemcpyAsync(c->h_states.p, states_rows, sizeof(double) * row * rows, cudaMemcpyHostToDevice,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_times.p, times_rows, sizeof(double) * nb * rows, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->h_dL.p, dL_rows, sizeof(double) * row * rows, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->lambda.p, lambda, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
+  std::vector<double> g(np);
+  cko_status s = adjoint_core(c, m, c->h_states.as<double>(), c->h_times.as<double>(), nb, chunk_len, chunk_len, sv,
+                              CKO_LOSS_USER, c->h_dL.as<double>(), nullptr, g.data(), work, err, true);
+  if (s != CKO_OK) return s;
+  CUDA_TRY(cudaMemcpyAsync(lambda, c->lambda.p, sizeof(double) * row, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (int j = 0; j < np; ++j) grad[j] += g[j];
+  for (int j = 0; j < np; ++j)
+    if (!std::isfinite(grad[j])) return fail(err, CKO_NON_FINITE, "parameter product of the model is not finite");
+  return ok(err);
+}
+
+cko_status cko_adjoint_chunk_solve(cko_ctx* c, const cko_model* m, const double* states, const double* times, int nb,
+                                   int nt, int step_hi, int chunk_len, const double* dL,
+                                   const cko_solver_choice* sv, double* lambda, double* grad, cko_work* work,
+                                   cko_error* err) {
+  if (!c || !m || !states || !times || !dL || !sv || !lambda || !grad) return fail(err, CKO_ERROR, "null argument");
+  if (!(chunk_len >= 1 && step_hi >= chunk_len && step_hi <= nt))
+    return fail(err, CKO_SHAPE_MISMATCH, "adjoint chunk: step range out of bounds");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n, lo = (size_t)(step_hi - chunk_len);
+  return chunk_reverse(c, m, states + lo * row, times + lo * nb, dL + lo * row, nb, chunk_len, sv, lambda, grad,
+                       work, err);
+}
+
+cko_status cko_adjoint_step_sequential(cko_ctx* c, const cko_model* m, const double* y_i, const double* y_prev,
+                                       const double* t_i, const double* t_prev, const double* dL_i, int nb,
+                                       const cko_solver_choice* sv, double* lambda, double* grad, cko_error* err) {
+  if (!c || !m || !y_i || !y_prev || !t_i || !t_prev || !dL_i || !sv || !lambda || !grad)
+    return fail(err, CKO_ERROR, "null argument");
+  if (nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint step: empty batch");
+  for (int b = 0; b < nb; ++b)
+    if (!(t_i[b] > t_prev[b])) return fail(err, CKO_SHAPE_MISMATCH, "adjoint step: dt must be positive");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  std::vector<double> st(2 * row), tt(2 * (size_t)nb), dl(2 * row, 0.0);
+  std::memcpy(st.data(), y_prev, sizeof(double) * row);
+  std::memcpy(st.data() + row, y_i, sizeof(double) * row);
+  std::memcpy(tt.data(), t_prev, sizeof(double) * nb);
+  std::memcpy(tt.data() + nb, t_i, sizeof(double) * nb);
+  std::memcpy(dl.data() + row, dL_i, sizeof(double) * row);
+  return chunk_reverse(c, m, st.data(), tt.data(), dl.data(), nb, 1, sv, lambda, grad, nullptr, err);
 }
 
 }  // extern "C"

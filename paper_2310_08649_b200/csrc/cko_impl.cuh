@@ -192,7 +192,7 @@ __device__ unsigned residual_phase(const FwdLaunch& a, const CtaWs& w, int step,
   for (int p = tid; p < c * L; p += T) {
     const int k = p / L, lb = p % L, b = lb0 + lb;
     const double t = a.times[(size_t)(step + 1 + k) * nb + b];
-    const double dt = t - a.times[(size_t)(step + k) * nb + b];
+    const double dt = a.dts ? a.dts[(size_t)(step + k) * nb + b] : t - a.times[(size_t)(step + k) * nb + b];
     SVec y = w.v(w.yy, p), h = w.v(w.hr, p);
     MD::rate(a.m, t, y, h, b);
     double s = 0.0;
@@ -245,7 +245,7 @@ __device__ unsigned jac_lu_phase(const FwdLaunch& a, const CtaWs& w, int step, i
   for (int p = threadIdx.x; p < c * L; p += T) {
     const int k = p / L, lb = p % L, b = lb0 + lb;
     const double t = a.times[(size_t)(step + 1 + k) * nb + b];
-    const double dt = t - a.times[(size_t)(step + k) * nb + b];
+    const double dt = a.dts ? a.dts[(size_t)(step + k) * nb + b] : t - a.times[(size_t)(step + k) * nb + b];
     SBlk J = w.b(w.lu, p);
     SVec y = w.v(w.yy, p);
     MD::jacobian(a.m, t, y, J, b);
@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(kMaxThreads) adj_kernel(AdjLaunch a) {
   CtaWs w = make_ws(a.slab, n, pcr);
   const size_t row = (size_t)nb * n;
   const double Lval = a.loss ? *a.loss : 0.0;
-  for (int idx = tid; idx < L * n; idx += T) a.lambda[(size_t)lb0 * n + idx] = 0.0;
+  if (!a.keep_lambda)
+    for (int idx = tid; idx < L * n; idx += T) a.lambda[(size_t)lb0 * n + idx] = 0.0;
   __syncthreads();
   int step_hi = a.nt;
   unsigned long long ord = 0;
@@ -486,11 +487,133 @@ __global__ void __launch_bounds__(256) vjp_kernel(DevModel m, const double* stat
   }
 }
 
+// ---------------------------------------------------------------------------
+// public single-chunk ops (integrate.cpp:269-297): thread per point (k, b)
+// ---------------------------------------------------------------------------
+struct PBlk {
+  double* p;
+  int n;
+  __device__ __forceinline__ double& operator()(int i, int j) const { return p[i * n + j]; }
+};
+
+// op 0 chunk_residual: out(k) = dy(k) - dy(k-1) - h(y_start + dy(k), t(k)) dt(k) (residual_into,
+// integrate.cpp:37-56), flags |= 1 when h is not finite. op 1 chunk_jacobian: out(k) = I - J dt
+// (jacobian_into, integrate.cpp:100-113), flags |= 1 when J is not finite (jacobian_state,
+// ode_model.cpp:126-133). yyb: (c, nb, n) scratch for y_start + dy.
+template <class MD>
+__global__ void chunk_op_kernel(DevModel m, int op, const double* __restrict__ ys, const double* __restrict__ dy,
+                                const double* __restrict__ t, const double* __restrict__ dt, int c, int nb,
+                                double* yyb, double* out, unsigned* flags) {
+  const int n = m.n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c * nb; p += gridDim.x * blockDim.x) {
+    const int k = p / nb, b = p % nb;
+    double* yy = yyb + (size_t)p * n;
+    const double* d = dy + (size_t)p * n;
+    for (int i = 0; i < n; ++i) yy[i] = xadd(ys[(size_t)b * n + i], d[i]);
+    const double dtv = dt[p];
+    bool fin = true;
+    if (op == 0) {
+      double* h = out + (size_t)p * n;
+      MD::rate(m, t[p], yy, h, b);
+      for (int i = 0; i < n; ++i) fin &= isfinite(h[i]);
+      for (int i = 0; i < n; ++i)
+        h[i] = k == 0 ? xsub(d[i], xmul(h[i], dtv)) : xsub(xsub(d[i], d[i - (ptrdiff_t)nb * n]), xmul(h[i], dtv));
+    } else {
+      PBlk J{out + (size_t)p * n * n, n};
+      MD::jacobian(m, t[p], yy, J, b);
+      for (int e = 0; e < n * n; ++e) fin &= isfinite(J.p[e]);
+      for (int e = 0; e < n * n; ++e) J.p[e] = xmul(-dtv, J.p[e]);
+      for (int i = 0; i < n; ++i) J(i, i) = xadd(J(i, i), 1.0);
+    }
+    if (!fin) atomicOr(flags, 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward Euler scheme: thread per lane, steps in order
+// ---------------------------------------------------------------------------
+// integrate_forward_euler (integrate.cpp:371-407): y_s = y_{s-1} + h(y_{s-1}, t_{s-1}) dt_s with the
+// reference's roundings; *bad = the first step whose state is not finite (min over lanes).
+template <class MD>
+__global__ void fe_forward_kernel(DevModel m, double* states, const double* times, int nb, int nt, double* hbuf,
+                                  int* bad) {
+  const int n = m.n;
+  const size_t row = (size_t)nb * n;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    MVec h{hbuf + (size_t)b * n};
+    int first_bad = INT_MAX;
+    for (int s = 1; s <= nt; ++s) {
+      const double* yp = states + (size_t)(s - 1) * row + (size_t)b * n;
+      double* y = states + (size_t)s * row + (size_t)b * n;
+      const double tp = times[(size_t)(s - 1) * nb + b];
+      const double dt = times[(size_t)s * nb + b] - tp;
+      MD::rate(m, tp, CVec{yp}, h, b);
+      bool fin = true;
+      for (int i = 0; i < n; ++i) {
+        const double v = xadd(yp[i], xmul(h[i], dt));
+        y[i] = v;
+        fin &= isfinite(v);
+      }
+      if (!fin && s < first_bad) first_bad = s;
+    }
+    if (first_bad != INT_MAX) atomicMin(bad, first_bad);
+  }
+}
+
+// The forward-Euler discrete adjoint (fe_chunk_core, adjoint.cpp:157-188), per lane from the top:
+// lambda += jump_m; w_m = lambda dt_m; lambda += dt_m J(y_{m-1}, t_{m-1})^T lambda (gemv_transpose's
+// order, adjoint.cpp:38-45). No solve. w_m goes to wq row m; the parameter product is evaluated at
+// (y_{m-1}, t_{m-1}) by the VJP kernels on row-shifted views. *bad |= 1 for a non-finite Jacobian
+// (jacobian_state, ode_model.cpp:126-133). Jb (nb, n, n) and tmp (nb, n) are scratch.
+template <class MD>
+__global__ void fe_adjoint_kernel(DevModel m, const double* states, const double* times, const double* dL,
+                                  const double* loss, int nb, int nt, double* lambda, double* Jbuf, double* tmp,
+                                  double* wq, unsigned* bad) {
+  const int n = m.n;
+  const size_t row = (size_t)nb * n;
+  const double Lval = loss ? *loss : 0.0;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    double* lam = lambda + (size_t)b * n;
+    double* Jb = Jbuf + (size_t)b * n * n;
+    double* tp = tmp + (size_t)b * n;
+    for (int i = 0; i < n; ++i) lam[i] = 0.0;
+    bool fin = true;
+    for (int ms = nt; ms >= 1; --ms) {
+      const double* ym = states + (size_t)ms * row + (size_t)b * n;
+      for (int i = 0; i < n; ++i)
+        lam[i] = xadd(lam[i], dL ? dL[(size_t)ms * row + (size_t)b * n + i] : (Lval > 0.0 ? ym[i] / Lval : 0.0));
+      const double t0 = times[(size_t)(ms - 1) * nb + b];
+      const double dt = times[(size_t)ms * nb + b] - t0;
+      double* w = wq + (size_t)ms * row + (size_t)b * n;
+      for (int i = 0; i < n; ++i) w[i] = xmul(lam[i], dt);
+      PBlk J{Jb, n};
+      MD::jacobian(m, t0, CVec{states + (size_t)(ms - 1) * row + (size_t)b * n}, J, b);
+      for (int e = 0; e < n * n; ++e) fin &= isfinite(Jb[e]);
+      for (int i = 0; i < n; ++i) tp[i] = 0.0;
+      for (int j = 0; j < n; ++j) {
+        const double vj = lam[j];
+        for (int i = 0; i < n; ++i) tp[i] = xadd(tp[i], xmul(Jb[j * n + i], vj));
+      }
+      for (int i = 0; i < n; ++i) lam[i] = xadd(lam[i], xmul(dt, tp[i]));
+    }
+    if (!fin) atomicOr(bad, 1u);
+  }
+}
+
 // Per-model launchers, defined by CKO_INSTANTIATE in cko_inst_*.cu.
 #define CKO_DECLARE(NAME)                                                                       \
   cudaError_t fwd_run_##NAME(const FwdLaunch& a, cudaStream_t st);                                 \
   cudaError_t fwd_occ_##NAME(int threads, int* blocks);                                            \
   cudaError_t preload_##NAME();                                                                    \
+  cudaError_t fe_forward_run_##NAME(const DevModel& m, double* states, const double* times, int nb,   \
+                                    int nt, double* hbuf, int* bad, cudaStream_t st);                  \
+  cudaError_t fe_adjoint_run_##NAME(const DevModel& m, const double* states, const double* times,     \
+                                    const double* dL, const double* loss, int nb, int nt,              \
+                                    double* lambda, double* Jb, double* tmp, double* wq,               \
+                                    unsigned* bad, cudaStream_t st);                                   \
+  cudaError_t chunk_op_run_##NAME(const DevModel& m, int op, const double* ys, const double* dy,       \
+                                  const double* t, const double* dt, int c, int nb, double* yyb,       \
+                                  double* out, unsigned* flags, cudaStream_t st);                      \
   cudaError_t adj_run_##NAME(const AdjLaunch& a, cudaStream_t st);                                 \
   cudaError_t vjp_run_##NAME(const DevModel& m, const double* states, const double* times,          \
                              const double* wq, int nb, int nt, double* scratch, cudaStream_t st);

@@ -246,6 +246,29 @@ cudaError_t preload_kernels() {
   return preload_node_kernels();
 }
 
+cudaError_t launch_chunk_op(const DevModel& m, int op, const double* ys, const double* dy, const double* t,
+                            const double* dt, int c, int nb, double* yyb, double* out, unsigned* flags,
+                            cudaStream_t st) {
+#define CALL(N) chunk_op_run_##N(m, op, ys, dy, t, dt, c, nb, yyb, out, flags, st)
+  CKO_SWITCH(m.kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_fe_forward(const DevModel& m, double* states, const double* times, int nb, int nt, double* hbuf,
+                              int* bad, cudaStream_t st) {
+#define CALL(N) fe_forward_run_##N(m, states, times, nb, nt, hbuf, bad, st)
+  CKO_SWITCH(m.kind, CALL)
+#undef CALL
+}
+
+cudaError_t launch_fe_adjoint(const DevModel& m, const double* states, const double* times, const double* dL,
+                              const double* loss, int nb, int nt, double* lambda, double* Jb, double* tmp,
+                              double* wq, unsigned* bad, cudaStream_t st) {
+#define CALL(N) fe_adjoint_run_##N(m, states, times, dL, loss, nb, nt, lambda, Jb, tmp, wq, bad, st)
+  CKO_SWITCH(m.kind, CALL)
+#undef CALL
+}
+
 cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st) {
   solve_kernel<<<a.grid, a.threads, 0, st>>>(a);
   return cudaGetLastError();

@@ -29,6 +29,8 @@ struct FwdLaunch {
   double* states;        // (nt+1, nb, n), row 0 = y0 on entry
   const double* times;   // (nt+1, nb)
   const double* dy_init; // optional (nc, nb, n): initial increments (newton_solve_chunk)
+  const double* dts;     // optional (nt, nb): explicit step sizes dt(s, b) = dts[(s-1) nb + b] instead of
+                         // t(s) - t(s-1) (newton_solve_chunk's independent dt_chunk; generic kernels only)
   int nb, nt, nc;
   double tol_a, tol_r;
   int max_iter;
@@ -56,7 +58,8 @@ struct AdjLaunch {
   int nb, nt, nc;
   int solver, n_switch;
   Slab slab;
-  double* lambda;        // (nb, n)
+  double* lambda;        // (nb, n): the carry; zeroed on entry unless keep_lambda (adjoint_chunk_solve)
+  int keep_lambda;       // generic kernels only
   double* wq;            // (nt+1, nb, n) quadrature weights lambda_m dt_m (row 0 unused)
   unsigned long long* sing_key;  // min over (chunk ordinal, r, b)
   int grid;
@@ -105,6 +108,14 @@ inline int pcr2_ws_bound(int n) { return 3 * n * n + 5 * n + 20; }
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
                         const GroupView& g, GridSync* gs, unsigned* status, cudaStream_t st);
 // In-place deterministic sum of v[0..cnt) over the ranks of the group.
+cudaError_t launch_chunk_op(const DevModel& m, int op, const double* ys, const double* dy, const double* t,
+                            const double* dt, int c, int nb, double* yyb, double* out, unsigned* flags,
+                            cudaStream_t st);
+cudaError_t launch_fe_forward(const DevModel& m, double* states, const double* times, int nb, int nt, double* hbuf,
+                              int* bad, cudaStream_t st);
+cudaError_t launch_fe_adjoint(const DevModel& m, const double* states, const double* times, const double* dL,
+                              const double* loss, int nb, int nt, double* lambda, double* Jb, double* tmp,
+                              double* wq, unsigned* bad, cudaStream_t st);
 cudaError_t preload_kernels();
 cudaError_t preload_node_kernels();
 cudaError_t launch_key_flag(const unsigned long long* key, double* v, cudaStream_t st);
