@@ -189,6 +189,31 @@ class Oracle:
         raise_for(rc, e)
         return x
 
+    # -- the reference's benchmark harness (reference only) -----------------------
+    def _text(self, fn, *args):
+        cap = 1 << 16
+        while True:
+            buf = C.create_string_buffer(cap)
+            e = abi.CkoError()
+            k = fn(*args, buf, cap, C.byref(e))
+            if k == -1:
+                raise_for(e.code or abi.CKO_ERROR, e)
+            if k >= 0:
+                return buf.value.decode()
+            cap = -k + 16
+
+    def study_csv(self, grid_text: str) -> str:
+        assert self.kind == "ref"
+        self.lib.ref_study_csv.restype = C.c_int
+        return self._text(self.lib.ref_study_csv, grid_text.encode())
+
+    def dump_trajectory(self, problem, n_unit, n_batch, n_time, n_chunk, solver="thomas", n_switch=1,
+                        integration="backward", t_max=0.0) -> str:
+        assert self.kind == "ref"
+        self.lib.ref_dump_trajectory.restype = C.c_int
+        return self._text(self.lib.ref_dump_trajectory, problem.encode(), n_unit, n_batch, n_time, n_chunk,
+                          solver.encode(), n_switch, integration.encode(), C.c_double(t_max))
+
     # -- forward Euler scheme (reference only) ----------------------------------
     def fe_gradient(self, model, y0, times, n_chunk, dL=None):
         assert self.kind == "ref"

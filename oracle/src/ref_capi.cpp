@@ -9,10 +9,13 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
+#include <string>
 #include <thread>
 #include <vector>
 
 #include "chunkode/adjoint.hpp"
+#include "chunkode/bench.hpp"
 #include "chunkode/integrate.hpp"
 #include "chunkode/linalg.hpp"
 #include "chunkode/models.hpp"
@@ -508,6 +511,53 @@ int ref_adjoint_chunk(const cko_model_desc* d, int op, const double* states, con
     return 0;
   } catch (...) {
     return map_exception(err);
+  }
+}
+
+// The reference's benchmark harness: run_study over a grid given as text
+// (bench.cpp:346-416) and dump_trajectory (bench.cpp:418-441), CSV into `out`.
+// Returns the CSV length, or -(needed length) when `cap` is too small, or -1
+// on an exception (message in err).
+static int put_text(const std::string& s, char* out, int cap) {
+  if (int(s.size()) + 1 > cap) return -int(s.size() + 1);
+  std::memcpy(out, s.data(), s.size());
+  out[s.size()] = 0;
+  return int(s.size());
+}
+
+int ref_study_csv(const char* grid_text, char* out, int cap, cko_error* err) {
+  try {
+    std::istringstream in(grid_text);
+    std::ostringstream os;
+    run_study(parse_grid_file(in), os, false);
+    fill(err, CKO_OK, "");
+    return put_text(os.str(), out, cap);
+  } catch (...) {
+    map_exception(err);
+    return -1;
+  }
+}
+
+int ref_dump_trajectory(const char* problem, int n_unit, int n_batch, int n_time, int n_chunk, const char* solver,
+                        int n_switch, const char* integration, double t_max, char* out, int cap, cko_error* err) {
+  try {
+    TrialConfig cfg;
+    cfg.problem = problem;
+    cfg.n_unit = n_unit;
+    cfg.n_batch = n_batch;
+    cfg.n_time = n_time;
+    cfg.n_chunk = n_chunk;
+    cfg.solver = solver;
+    cfg.n_switch = n_switch;
+    cfg.integration = integration;
+    cfg.t_max = t_max;
+    std::ostringstream os;
+    dump_trajectory(cfg, os);
+    fill(err, CKO_OK, "");
+    return put_text(os.str(), out, cap);
+  } catch (...) {
+    map_exception(err);
+    return -1;
   }
 }
 

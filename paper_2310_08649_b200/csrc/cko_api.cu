@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/chunkode_b200.h"
@@ -152,6 +153,8 @@ struct cko_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;  // trajectory downloads overlapping the adjoint
+  cudaEvent_t fwd_done = nullptr;
   int sms = 0;
   // workspace pool
   Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
@@ -247,6 +250,8 @@ cko_status cko_ctx_destroy(cko_ctx* c) {
   for (cudaEvent_t& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->fwd_done) cudaEventDestroy(c->fwd_done);
   delete c;
   return CKO_OK;
 }
@@ -1080,12 +1085,30 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
   CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
   if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
   if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err)) return s;
-  if (states_out) {
-    CUDA_TRY(cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost,
-                             c->stream));
-  }
-  return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out, grad_out, bwd,
-                      err);
+  if (!states_out)
+    return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out, grad_out,
+                        bwd, err);
+  // The trajectory download overlaps the adjoint (both only read d_states): a helper thread copies it on
+  // the context's copy stream (a pageable destination blocks the issuing thread, not the adjoint's
+  // launches), while this thread runs the adjoint on the compute stream.
+  if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->fwd_done) CUDA_TRY(cudaEventCreateWithFlags(&c->fwd_done, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(c->fwd_done, c->stream));
+  cudaError_t copy_err = cudaSuccess;
+  std::thread copier([&] {
+    copy_err = cudaSetDevice(c->device);
+    if (copy_err == cudaSuccess) copy_err = cudaStreamWaitEvent(c->copy_stream, c->fwd_done, 0);
+    if (copy_err == cudaSuccess)
+      copy_err = cudaMemcpyAsync(states_out, d_states, sizeof(double) * row * (nt + 1), cudaMemcpyDeviceToHost,
+                                 c->copy_stream);
+    if (copy_err == cudaSuccess) copy_err = cudaStreamSynchronize(c->copy_stream);
+  });
+  cko_status s = adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out,
+                              grad_out, bwd, err);
+  copier.join();
+  if (s != CKO_OK) return s;
+  if (copy_err != cudaSuccess) return fail(err, CKO_CUDA, "trajectory D2H: %s", cudaGetErrorString(copy_err));
+  return CKO_OK;
 }
 
 cko_status cko_traj_states(const cko_traj* t, const double** d_states, int* nb, int* nt, int* n) {
