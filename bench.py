@@ -396,9 +396,18 @@ def main():
     from paper_2310_08649_b200.errors import raise_for
 
     rank, world, local = dist_env()
+    # CKO_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo process group -- exercises the multi-rank
+    # plumbing (self-launch, IPC group, per-iteration exchange, max-over-ranks timing) on a one-GPU box;
+    # the contexts time-slice the GPU, so its timings mean nothing.
+    one_gpu = os.environ.get("CKO_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     model, y0, times = mds_workload(args, world, rank)
     nb, nt, n = y0.shape[0], args.nt, model.state_size
     _, _, nb_total = lane_split(args, world, rank)
@@ -461,7 +470,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if one_gpu else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = nb_total * nt / (ms * 1e-3)
@@ -490,7 +499,7 @@ def main():
         torch.cuda.synchronize()
         e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         if world > 1:
-            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            t = torch.tensor([e_ms], device="cpu" if one_gpu else "cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": nb_total * nt / (e_ms * 1e-3), "unit": "series*steps/s",
