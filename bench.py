@@ -313,6 +313,49 @@ def c3_pcr_vs_sequential(ctx, reps=2):
     return out
 
 
+def c4_training_step(ctx, reps=2, ncs=(10, 20, 100), cpu_steps=100):
+    """North-star C4: neural ODE, state 8, hidden width 128 (18 824 parameters, MLP rate on DMMA),
+    nb = 256, nt = 2000, one adjoint training step (forward + adjoint + parameter gradient) through the public
+    API with host buffers; n_chunk sweep, wall clock around the synchronous calls. cpu_baseline: the compiled
+    reference integrator + adjoint running the same NodeWide model (oracle/src/ref_models.hpp), single thread,
+    on the first `cpu_steps` steps of the same grid."""
+    import paper_2310_08649_b200 as P
+    from paper_2310_08649_b200 import api
+    nb, nt = 256, 2000
+    m = P.build_node_wide(8, 128, nb)
+    grid = api.TimeGrid.uniform(nt, nb, 1.0)
+    y0 = np.zeros((nb, 8))
+    out = {"workload": "C4 neural ODE n=8, W=128, nb=256, nt=2000, t_max=1, thomas, forward+adjoint+gradient"}
+    best = None
+    for nc in ncs:
+        sv = api.SolverChoice(0, 1)
+        api.gradient_adjoint(m, y0, grid, nc, solver=sv, ctx=ctx)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = api.gradient_adjoint(m, y0, grid, nc, solver=sv, ctx=ctx)
+        sec = (time.perf_counter() - t0) / reps
+        v = nb * nt / sec
+        out[f"n_chunk={nc}"] = {"seconds": sec, "series_steps_per_s": v,
+                                "newton_iterations": r.trajectory.work.newton_iterations, "loss": r.loss,
+                                "launches": ctx.last_launches() if hasattr(ctx, "last_launches") else None}
+        if best is None or v > best[1]:
+            best = (nc, v)
+    out["best"] = {"n_chunk": best[0], "series_steps_per_s": best[1]}
+    try:
+        from oracle import load_ref, ref_available
+        if ref_available():
+            ts = grid.times[:cpu_steps + 1]
+            t0 = time.perf_counter()
+            load_ref().gradient(m, y0, ts, min(20, cpu_steps))
+            sec = time.perf_counter() - t0
+            out["cpu_baseline"] = {"value": nb * cpu_steps / sec, "unit": "series*steps/s", "cores": 1,
+                                   "kind": "reference", "sample": f"all {nb} lanes x the first {cpu_steps} steps, "
+                                   f"n_chunk={min(20, cpu_steps)}, single thread, {sec:.1f} s"}
+    except Exception as ex:  # the checker build is missing on this box
+        out["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    return out
+
+
 def c2_solver_family(args, local, nt_s=500, reps=2):
     """The headline workload's chunked solver family on this GPU, bounded sample (nb lanes x nt_s steps,
     same dt), device-resident through the C ABI and timed with the kernels' own CUDA events: Thomas (the
@@ -363,6 +406,66 @@ def c2_solver_family(args, local, nt_s=500, reps=2):
     L.cko_ctx_enable_timing(ctx.h, 0)
     out["sample"] = f"nb={nb} x nt={nt_s} (dt as the full grid), device-resident, kernel time"
     return out
+
+
+def north_star_strong(args, ctx, world, rank, stream, hbm_peak, reps=3, warmup=2):
+    """The north-star target (BASELINE.json): the 1000-series, 10k-step MDS case split over all ranks of this
+    run (strong scaling, 1000/world lanes per GPU), forward + adjoint per step, device-resident, timed with
+    CUDA events on the compute stream, max over ranks; HBM fraction from the compulsory bytes
+    B_alg = 16 n + 16 per series*step; loss / gradient / counters checked against the
+    compiled reference's full-size run."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2310_08649_b200 import abi, api
+    from paper_2310_08649_b200._native import lib
+    from paper_2310_08649_b200.errors import raise_for
+    sa = argparse.Namespace(**vars(args))
+    sa.scaling, sa.nb_total = "strong", 1000
+    model, y0, times = mds_workload(sa, world, rank)
+    nb, nt, n = y0.shape[0], sa.nt, model.state_size
+    L = lib()
+    dm = ctx.model(model)
+    d_y0 = torch.from_numpy(y0).cuda()
+    d_times = torch.from_numpy(times).cuda()
+    d_states = torch.empty((nt + 1, nb * n), dtype=torch.float64, device="cuda")
+    st, sv = api.NewtonSettings().c(), api.SolverChoice(SOLVER_ID[sa.solver], sa.n_switch).c()
+    grad = np.zeros(model.params.size)
+    loss = C.c_double()
+    wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+
+    def step():
+        raise_for(L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()),
+                                          nb, nt, sa.n_chunk, C.byref(st), C.byref(sv),
+                                          C.c_void_p(d_states.data_ptr()), C.byref(wf), C.byref(e)), e)
+        raise_for(L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()), C.c_void_p(d_times.data_ptr()),
+                                          nb, nt, sa.n_chunk, C.byref(sv), abi.CKO_LOSS_FROBENIUS, None,
+                                          C.byref(loss), abi.dptr(grad), C.byref(wb), C.byref(e)), e)
+    for _ in range(warmup):
+        step()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(reps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / reps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cpu" if os.environ.get("CKO_BENCH_ONE_GPU") == "1"
+                         else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    v = 1000 * nt / (ms * 1e-3)
+    b_alg = 16 * n + 16
+    return {"workload": f"C2 MDS n={n}, 1000 series over {world} GPU(s) ({nb} lanes on rank 0), nt={nt}, "
+                        f"{sa.solver} n_chunk={sa.n_chunk}, forward+adjoint", "value": v, "unit": "series*steps/s",
+            "ms_per_step": ms, "steps": reps, "warmup": warmup,
+            "hbm": {"achieved_gbs": v * b_alg / 1e9, "peak_gbs": hbm_peak, "frac": v * b_alg / 1e9 / hbm_peak,
+                    "alg_bytes_per_series_step": b_alg},
+            "parity": golden_parity(sa, 1000, loss.value, grad, wf, wb)}
 
 
 # ---------------------------------------------------------------------------
@@ -507,6 +610,21 @@ def main():
                "d2h_bytes_per_step": int(grad.size * 8 + 8), "ms_per_step": e_ms,
                "path": "cko_gradient_adjoint (C ABI, pinned host y0/times -> loss + gradient)"}
 
+    hbm_peak = 6536.7
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        peak_src = "fallback"
+    # the north-star target: 1000 series over the ranks of this run (all ranks take part)
+    if world > 1 or args.scaling == "strong" or nb_total != 1000:
+        try:
+            ns_line = north_star_strong(args, ctx, world, rank, stream, hbm_peak)
+        except Exception as ex:  # side measurement only
+            ns_line = {"error": str(ex)[:200]}
+    else:
+        ns_line = None  # this run IS the 1000-series configuration: filled from the main line below
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -517,12 +635,6 @@ def main():
     kern = {"fwd_kernel": rec["fwd"] / k, "adj_kernel": rec["adj"] / k, "vjp_kernels": rec["vjp"] / k,
             "loss_kernels": rec["loss"] / k}
     dom = max(kern, key=kern.get)
-    hbm_peak = 6536.7
-    try:
-        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
-        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        peak_src = "fallback"
     units = nb * nt  # series*steps per launch on this rank
     bytes_per = {"fwd_kernel": 8 * n + 8, "adj_kernel": 8 * n + 8 + 8 * n, "vjp_kernels": 8 * n + 8 + 8 * n,
                  "loss_kernels": 8 * n}[dom]
@@ -554,6 +666,14 @@ def main():
         "e2e": e2e,
     }
     line["kernel_generation"] = L.cko_ctx_kernel_generation_used(ctx.h)
+    if ns_line is None:
+        b_alg = 16 * n + 16
+        ns_line = {"workload": "this run (1000 series on 1 GPU)", "value": value, "unit": "series*steps/s",
+                   "ms_per_step": ms, "hbm": {"achieved_gbs": value * b_alg / 1e9, "peak_gbs": hbm_peak,
+                                              "frac": value * b_alg / 1e9 / hbm_peak,
+                                              "alg_bytes_per_series_step": b_alg},
+                   "parity": line["parity"]}
+    line["north_star_1000_series"] = ns_line
     traffic = load_traffic(dom, args)
     if traffic is not None:
         line["roofline"]["traffic"] = traffic["bytes_per_launch"]
@@ -567,6 +687,10 @@ def main():
             line["c3_pcr_vs_sequential"] = c3_pcr_vs_sequential(api.Context(local))
         except Exception as ex:
             line["c3_pcr_vs_sequential"] = {"error": str(ex)[:200]}
+        try:
+            line["c4_training_step"] = c4_training_step(api.Context(local))
+        except Exception as ex:
+            line["c4_training_step"] = {"error": str(ex)[:200]}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_single(args)
