@@ -33,7 +33,8 @@ def _check(got, want):
     assert rel_max(got.gradient, want.grad) <= TOL
 
 
-PCR2_KINDS = {"lin3", "mds_small", "chaboche", "scalar", "constant"}  # block size <= 8
+PCR2_KINDS = {"lin3", "mds_small", "chaboche", "scalar", "constant",  # block size <= 8 (thread per point)
+              "mds"}  # n = 20: warp-cooperative sweeps (cko_pcrw.cuh)
 
 
 @pytest.mark.parametrize("name", ALL_CASES)
@@ -193,3 +194,19 @@ def test_mds_wide_ctas(port, nb, nt, nc):
     got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, ctx=ctx)
     assert ctx.kernel_generation_used() == 2
     _check(got, want)
+
+
+@pytest.mark.parametrize("nc", [1, 2, 3, 5, 16, 33, 100, 128])
+@pytest.mark.parametrize("solver", [(1, 1), (2, 1), (2, 3), (2, 0)])
+def test_pcrw_mds20_chunks(port, nc, solver):
+    """North-star block size (MDS, n = 20) under PCR / hybrid on the warp-cooperative generation-2 kernels:
+    power-of-two and ragged partitions (100 = 64 + 32 + 4, 33 = 32 + 1), lanes below and above the CTA count."""
+    for nb in (3, 200):
+        m = P.build_mass_damper_spring(10, nb)
+        y0 = np.zeros((nb, 20))
+        t = uniform_times(256, nb, 256 * 1e-6)
+        want = port.gradient(m, y0, t, nc, solver=solver)
+        ctx = _ctx(2)
+        got = api.gradient_adjoint(m, y0, api.TimeGrid(t), nc, solver=api.SolverChoice(*solver), ctx=ctx)
+        _check(got, want)
+        assert ctx.kernel_generation_used() == 2
