@@ -356,11 +356,12 @@ def c4_training_step(ctx, reps=2, ncs=(10, 20, 100), cpu_steps=100):
     return out
 
 
-def c2_solver_family(args, local, nt_s=500, reps=2):
-    """The headline workload's chunked solver family on this GPU, bounded sample (nb lanes x nt_s steps,
-    same dt), device-resident through the C ABI and timed with the kernels' own CUDA events: Thomas (the
-    bench line's solver) next to PCR and hybrid at their best measured chunk, so the metric's PCR member is
-    on record (~40x the fp64 work of Thomas at n = 20)."""
+def c2_solver_family(args, local, nt_s=None, reps=1):
+    """The headline workload's chunked solver family on this GPU at FULL size (nb lanes x nt steps, the bench
+    grid), device-resident through the C ABI and timed with the kernels' own CUDA events: Thomas/n_chunk (the
+    bench line's solver) next to PCR/100 and hybrid/16 on the generation-2 warp-cooperative PCR kernels
+    (cko_pcrw.cuh), so the metric's PCR member is on record at the headline shape (PCR
+    does ~40x the fp64 work of Thomas at n = 20 and pays only when the batch cannot fill the GPU)."""
     import ctypes as C
 
     import torch
@@ -369,6 +370,7 @@ def c2_solver_family(args, local, nt_s=500, reps=2):
     from paper_2310_08649_b200 import abi, api
     from paper_2310_08649_b200._native import lib
     from paper_2310_08649_b200.errors import raise_for
+    nt_s = nt_s or args.nt
     L = lib()
     ctx = api.Context(local)
     m = P.build_mass_damper_spring(args.n_unit, args.nb)
@@ -384,7 +386,7 @@ def c2_solver_family(args, local, nt_s=500, reps=2):
     kms = (C.c_double * 4)()
     L.cko_ctx_enable_timing(ctx.h, 1)
     out = {}
-    for name, kind, nc in (("thomas", 0, args.n_chunk), ("pcr", 1, 4), ("hybrid", 2, 16)):
+    for name, kind, nc in (("thomas", 0, args.n_chunk), ("pcr", 1, 100), ("hybrid", 2, 16)):
         sv = api.SolverChoice(kind, 1).c()
         tot = 0.0
         for it in range(reps + 1):
@@ -404,7 +406,7 @@ def c2_solver_family(args, local, nt_s=500, reps=2):
         out[name] = {"n_chunk": nc, "series_steps_per_s": nb * nt_s / (ms * 1e-3), "kernel_ms": ms,
                      "kernel_generation": ctx.kernel_generation_used()}
     L.cko_ctx_enable_timing(ctx.h, 0)
-    out["sample"] = f"nb={nb} x nt={nt_s} (dt as the full grid), device-resident, kernel time"
+    out["sample"] = f"nb={nb} x nt={nt_s} (the full grid), device-resident, kernel time, {reps} timed pass(es)"
     return out
 
 
