@@ -96,10 +96,23 @@ typedef enum {
   CKO_MODEL_MDS = 3,           /* models_mds.cpp:16-97     n=2u, p=[K(u),C(u),M(u),f_a,T(nb)] */
   CKO_MODEL_CHABOCHE = 4,      /* models_chaboche.cpp:19-194 n=2+u,
                                   p=[E,n,eta,s0,Kinf,tau,C(u),gamma(u),eps_a(nb),T]  */
-  CKO_MODEL_NODE = 5           /* models_node.cpp:13-205 (width = u+1) and the wide
+  CKO_MODEL_NODE = 5,          /* models_node.cpp:13-205 (width = u+1) and the wide
                                   variant: n=u, p=[W1(Wx(u+1)),b1(W),
                                   W2(WxW),b2(W),W3(uxW),b3(u)]                        */
+  CKO_MODEL_NEURON = 6         /* models_neuron.cpp:16-156 n=4u, p=[14 per-unit
+                                  segments (C,g_Na,E_Na,g_K,E_K,g_L,E_L,m_inf,tau_m,
+                                  h_inf,tau_h,n_inf,tau_n,g_C), I_a(nb), T(u)]; u <= 8 */
 } cko_model_kind;
+
+/* JacobianStrategy (ode_model.hpp:14): analytic = the device twins' hand-written
+ * Jacobians; forward_ad = device dual numbers, eight columns per pass
+ * (ode_model.hpp:132-151); finite_difference = central differences
+ * (ode_model.cpp:44-66). Non-analytic strategies run the generic kernels. */
+typedef enum {
+  CKO_JACOBIAN_ANALYTIC = 0,
+  CKO_JACOBIAN_FORWARD_AD = 1,
+  CKO_JACOBIAN_FINITE_DIFFERENCE = 2
+} cko_jacobian_strategy;
 
 /* Flat model description, the C image of an OdeModel's identity:
  * kind + dims + params() (ode_model.hpp:35). n_batch_model is the batch width
@@ -300,6 +313,8 @@ int cko_ctx_last_launches(cko_ctx* ctx);
  * cko_ctx_kernel_generation_used reports what the last forward / adjoint ran. */
 cko_status cko_ctx_set_kernel_generation(cko_ctx* ctx, int gen);
 int cko_ctx_kernel_generation_used(cko_ctx* ctx);
+/* JacobianStrategy of the context's following calls (default analytic). */
+cko_status cko_ctx_set_jacobian_strategy(cko_ctx* ctx, int strategy);
 /* FP64 FMA-pipe throughput probe (dependent-chain-free DFMA stream over all
  * SMs); writes TFLOP/s (2 flops per DFMA). The FP64 roof for the roofline. */
 cko_status cko_probe_fp64_tflops(cko_ctx* ctx, double* tflops, cko_error* err);

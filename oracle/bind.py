@@ -189,6 +189,11 @@ class Oracle:
         raise_for(rc, e)
         return x
 
+    def set_jacobian_strategy(self, strategy: str) -> None:
+        """JacobianStrategy of the following reference calls on this thread."""
+        assert self.kind == "ref"
+        self.lib.ref_set_jacobian_strategy({"analytic": 0, "forward_ad": 1, "finite_difference": 2}[strategy])
+
     # -- the reference's benchmark harness (reference only) -----------------------
     def _text(self, fn, *args):
         cap = 1 << 16

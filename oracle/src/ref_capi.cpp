@@ -27,6 +27,8 @@ using namespace chunkode;
 
 namespace {
 
+thread_local JacobianStrategy g_strategy = JacobianStrategy::analytic;  // ref_set_jacobian_strategy
+
 void fill(cko_error* e, int code, const char* msg) {
   if (!e) return;
   std::memset(e, 0, sizeof(*e));
@@ -84,6 +86,7 @@ std::unique_ptr<OdeModel> build(const cko_model_desc* d) {
     case CKO_MODEL_CONSTANT_RATE: m = build_constant_rate(0.0); break;
     case CKO_MODEL_MDS: m = build_mass_damper_spring(d->n_unit, nb); break;
     case CKO_MODEL_CHABOCHE: m = build_chaboche(d->n_unit, nb); break;
+    case CKO_MODEL_NEURON: m = build_neuron(d->n_unit, nb); break;
     case CKO_MODEL_LIN3: m = std::make_unique<cko_ref::Lin3>(cko_ref::Lin3::default_params(), nb); break;
     case CKO_MODEL_NODE:
       if (d->width == d->n_unit + 1)
@@ -127,6 +130,13 @@ TimeGrid grid_of(const double* times, int nb, int nt) {
 
 extern "C" {
 
+// JacobianStrategy of the following reference calls on this thread (0 analytic, 1 forward_ad,
+// 2 finite_difference).
+void ref_set_jacobian_strategy(int s) {
+  g_strategy = s == 1 ? JacobianStrategy::forward_ad
+               : s == 2 ? JacobianStrategy::finite_difference : JacobianStrategy::analytic;
+}
+
 // Default parameters of the reference builders (models.hpp:14-41); for NODE
 // the `seed` drives mt19937_64 exactly as the reference does.
 int ref_default_params(const cko_model_desc* d, unsigned long long seed, double* out, int cap,
@@ -161,7 +171,7 @@ int ref_forward(const cko_model_desc* d, const double* y0, const double* times, 
     std::memcpy(Y0.data(), y0, sizeof(double) * Y0.size());
     NewtonSettings ns{st->tol_a, st->tol_r, st->max_iter};
     Trajectory tr =
-        integrate_backward_euler(*m, Y0, grid_of(times, nb, nt), n_chunk, ns, solver_of(sv));
+        integrate_backward_euler(*m, Y0, grid_of(times, nb, nt), n_chunk, ns, solver_of(sv), g_strategy);
     std::memcpy(states_out, tr.states.data(), sizeof(double) * tr.states.size());
     put_work(work, tr.work);
     fill(err, CKO_OK, "");
@@ -192,7 +202,7 @@ int ref_adjoint(const cko_model_desc* d, const double* states, const double* tim
     }
     WorkCounters w;
     auto [L, grad] = adjoint_backward(*m, tr, n_chunk, loss, Scheme::backward_euler, solver_of(sv),
-                                      JacobianStrategy::analytic, &w);
+                                      g_strategy, &w);
     if (loss_out) *loss_out = L;
     std::memcpy(grad_out, grad.data(), sizeof(double) * grad.size());
     put_work(bwd, w);
@@ -242,7 +252,7 @@ int ref_fe_adjoint(const cko_model_desc* d, const double* states, const double* 
     }
     WorkCounters w;
     auto [L, grad] = adjoint_backward(*m, tr, n_chunk, loss, Scheme::forward_euler, SolverChoice{},
-                                      JacobianStrategy::analytic, &w);
+                                      g_strategy, &w);
     if (loss_out) *loss_out = L;
     std::memcpy(grad_out, grad.data(), sizeof(double) * grad.size());
     put_work(bwd, w);
@@ -266,11 +276,11 @@ int ref_gradient_adjoint(const cko_model_desc* d, const double* y0, const double
     NewtonSettings ns{st->tol_a, st->tol_r, st->max_iter};
     const auto grid = grid_of(times, nb, nt);
     const auto t0 = std::chrono::steady_clock::now();
-    Trajectory tr = integrate_backward_euler(*m, Y0, grid, n_chunk, ns, solver_of(sv));
+    Trajectory tr = integrate_backward_euler(*m, Y0, grid, n_chunk, ns, solver_of(sv), g_strategy);
     const auto t1 = std::chrono::steady_clock::now();
     WorkCounters w;
     auto [L, grad] = adjoint_backward(*m, tr, n_chunk, loss_frobenius(), Scheme::backward_euler,
-                                      solver_of(sv), JacobianStrategy::analytic, &w);
+                                      solver_of(sv), g_strategy, &w);
     const auto t2 = std::chrono::steady_clock::now();
     if (seconds) {
       seconds[0] = std::chrono::duration<double>(t1 - t0).count();
@@ -416,7 +426,7 @@ int ref_model_eval(const cko_model_desc* d, int what, const double* t, const dou
       std::memcpy(out, o.data(), sizeof(double) * o.size());
     } else if (what == 1) {
       BatchedBlockArray o(c, nb, n);
-      jacobian_state(*m, T, Y, JacobianStrategy::analytic, o);
+      jacobian_state(*m, T, Y, g_strategy, o);
       std::memcpy(out, o.data(), sizeof(double) * o.size());
     } else {
       BatchedChunkVector W(c, nb, n);
@@ -453,13 +463,13 @@ int ref_chunk_op(const cko_model_desc* d, int op, const double* y_start, double*
       std::memcpy(out, o.data(), sizeof(double) * o.size());
     } else if (op == 1) {
       BlockBidiagonalSystem sys(c, nb, n);
-      chunk_jacobian(*m, ys, D, T, DT, JacobianStrategy::analytic, sys);
+      chunk_jacobian(*m, ys, D, T, DT, g_strategy, sys);
       std::memcpy(out, sys.diag.data(), sizeof(double) * sys.diag.size());
       if (out2 && c > 1) std::memcpy(out2, sys.offdiag.data(), sizeof(double) * sys.offdiag.size());
     } else {
       WorkCounters w;
       NewtonSettings ns{st->tol_a, st->tol_r, st->max_iter};
-      const int it = newton_solve_chunk(*m, ys, D, T, DT, ns, solver_of(sv), JacobianStrategy::analytic, &w, 1);
+      const int it = newton_solve_chunk(*m, ys, D, T, DT, ns, solver_of(sv), g_strategy, &w, 1);
       std::memcpy(dy, D.data(), sizeof(double) * D.size());
       if (iters) *iters = it;
       put_work(work, w);
@@ -494,7 +504,7 @@ int ref_adjoint_chunk(const cko_model_desc* d, int op, const double* states, con
       Array2d G(nt + 1, nb * n);
       std::memcpy(G.data(), dL, sizeof(double) * G.size());
       WorkCounters w;
-      adjoint_chunk_solve(*m, tr, step_hi, chunk_len, G, state, solver_of(sv), JacobianStrategy::analytic, &w);
+      adjoint_chunk_solve(*m, tr, step_hi, chunk_len, G, state, solver_of(sv), g_strategy, &w);
       put_work(work, w);
     } else {
       Array2d yi(nb, n), yp(nb, n), g(nb, n);
@@ -503,7 +513,7 @@ int ref_adjoint_chunk(const cko_model_desc* d, int op, const double* states, con
       std::memcpy(g.data(), dL + size_t(nb) * n, sizeof(double) * g.size());
       adjoint_step_sequential(*m, yi, yp, std::span<const double>(times + nb, nb),
                               std::span<const double>(times, nb), g, state, solver_of(sv),
-                              JacobianStrategy::analytic);
+                              g_strategy);
     }
     std::memcpy(lambda, state.lambda.data(), sizeof(double) * state.lambda.size());
     std::memcpy(grad, state.grad.data(), sizeof(double) * state.grad.size());

@@ -9,5 +9,5 @@ from . import abi, errors, models  # noqa: F401
 from .errors import *  # noqa: F401,F403
 from .models import (  # noqa: F401
     Model, build_chaboche, build_constant_rate, build_lin3, build_mass_damper_spring,
-    build_neural_ode, build_node_wide, build_problem, build_scalar_decay, linspace,
+    build_neural_ode, build_neuron, build_node_wide, build_problem, build_scalar_decay, linspace,
 )

@@ -72,6 +72,7 @@ def lib() -> C.CDLL:
         "cko_adjoint_chunk_solve": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, dp, P(S), dp, dp, P(W),
                                      P(E)], C.c_int),
         "cko_adjoint_step_sequential": ([vp, vp, dp, dp, dp, dp, dp, C.c_int, P(S), dp, dp, P(E)], C.c_int),
+        "cko_ctx_set_jacobian_strategy": ([vp, C.c_int], C.c_int),
         "cko_fe_forward": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, dp, P(W), P(E)], C.c_int),
         "cko_fe_adjoint_host": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, dp, P(W), P(E)],
                                 C.c_int),
@@ -95,5 +96,5 @@ EXPORTS = [
     "cko_newton_solve_chunk", "cko_ctx_enable_timing", "cko_ctx_last_kernel_ms", "cko_ctx_last_launches",
     "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open", "cko_ctx_set_kernel_generation",
     "cko_ctx_kernel_generation_used", "cko_chunk_residual", "cko_chunk_jacobian", "cko_adjoint_chunk_solve",
-    "cko_adjoint_step_sequential", "cko_fe_forward", "cko_fe_adjoint_host",
+    "cko_adjoint_step_sequential", "cko_fe_forward", "cko_fe_adjoint_host", "cko_ctx_set_jacobian_strategy",
 ]

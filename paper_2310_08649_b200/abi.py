@@ -28,6 +28,11 @@ CKO_MODEL_LIN3 = 2
 CKO_MODEL_MDS = 3
 CKO_MODEL_CHABOCHE = 4
 CKO_MODEL_NODE = 5
+CKO_MODEL_NEURON = 6
+
+CKO_JACOBIAN_ANALYTIC = 0
+CKO_JACOBIAN_FORWARD_AD = 1
+CKO_JACOBIAN_FINITE_DIFFERENCE = 2
 
 CKO_LOSS_FROBENIUS = 0
 CKO_LOSS_USER = 1

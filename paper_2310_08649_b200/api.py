@@ -200,6 +200,12 @@ class Context:
         if lib().cko_ctx_set_kernel_generation(self.h, int(gen)) != 0:
             raise ValueError(f"kernel generation must be 1 or 2, got {gen}")
 
+    def set_jacobian_strategy(self, strategy) -> None:
+        """JacobianStrategy of the following calls: 'analytic', 'forward_ad', 'finite_difference' (or 0/1/2)."""
+        k = _STRATEGY[strategy] if isinstance(strategy, str) else int(strategy)
+        if lib().cko_ctx_set_jacobian_strategy(self.h, k) != 0:
+            raise ValueError(f"unknown Jacobian strategy {strategy!r}")
+
     def kernel_generation_used(self) -> int:
         """Kernel generation the last forward / adjoint call ran (1 or 2)."""
         return int(lib().cko_ctx_kernel_generation_used(self.h))
@@ -218,6 +224,26 @@ class Context:
                 self._models.clear()
             self._models[key] = dm
         return dm
+
+
+_STRATEGY = {"analytic": abi.CKO_JACOBIAN_ANALYTIC, "forward_ad": abi.CKO_JACOBIAN_FORWARD_AD,
+             "finite_difference": abi.CKO_JACOBIAN_FINITE_DIFFERENCE}
+
+
+class _Strategy:
+    """Run one call under a JacobianStrategy (ode_model.hpp:14), restoring analytic afterwards."""
+
+    def __init__(self, ctx: "Context", strategy):
+        self.ctx, self.strategy = ctx, strategy
+
+    def __enter__(self):
+        if self.strategy not in ("analytic", 0):
+            self.ctx.set_jacobian_strategy(self.strategy)
+        return self.ctx
+
+    def __exit__(self, *exc):
+        if self.strategy not in ("analytic", 0):
+            self.ctx.set_jacobian_strategy("analytic")
 
 
 _tls = threading.local()
@@ -241,7 +267,7 @@ def _f64(a) -> np.ndarray:
 # ---------------------------------------------------------------------------
 def integrate_backward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int,
                              settings: NewtonSettings | None = None, solver: SolverChoice | None = None,
-                             ctx: Context | None = None) -> Trajectory:
+                             ctx: Context | None = None, strategy: str = "analytic") -> Trajectory:
     settings = settings or NewtonSettings()
     solver = solver or SolverChoice()
     y0 = _f64(y0)
@@ -254,8 +280,9 @@ def integrate_backward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int,
     states = np.zeros((nt + 1, nb * n))
     w, e = abi.CkoWork(), abi.CkoError()
     st, sv = settings.c(), solver.c()
-    rc = lib().cko_be_forward(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
-                              C.byref(st), C.byref(sv), dptr(states), None, C.byref(w), C.byref(e))
+    with _Strategy(ctx, strategy):
+        rc = lib().cko_be_forward(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
+                                  C.byref(st), C.byref(sv), dptr(states), None, C.byref(w), C.byref(e))
     raise_for(rc, e)
     return Trajectory(states, grid, nb, n, WorkCounters.from_c(w))
 
@@ -287,7 +314,7 @@ def integrate_forward_euler(model: Model, y0, grid: TimeGrid, n_chunk: int = 1,
 
 def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpec | None = None,
                      solver: SolverChoice | None = None, work: WorkCounters | None = None,
-                     ctx: Context | None = None, scheme: str = Scheme.backward_euler):
+                     ctx: Context | None = None, scheme: str = Scheme.backward_euler, strategy: str = "analytic"):
     """Returns (loss, gradient) like adjoint.hpp:63-66; `work` (if given) receives the backward counters."""
     loss = loss or loss_frobenius()
     solver = solver or SolverChoice()
@@ -309,6 +336,8 @@ def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpe
         dL = _f64(loss.state_gradient(traj))
         if dL.shape != traj.states.shape:
             raise ShapeMismatch("loss gradient: output must be shaped like the trajectory states")
+    strat = _Strategy(ctx, strategy)
+    strat.__enter__()
     if scheme == Scheme.forward_euler:
         rc = lib().cko_fe_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
                                        traj.n_batch, traj.n_time, int(n_chunk), kind, dptr(dL), C.byref(L),
@@ -317,6 +346,7 @@ def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpe
         rc = lib().cko_be_adjoint_host(ctx.h, ctx.model(model), dptr(_f64(traj.states)), dptr(traj.grid.times),
                                        traj.n_batch, traj.n_time, int(n_chunk), C.byref(sv), kind, dptr(dL),
                                        C.byref(L), dptr(grad), C.byref(w), C.byref(e))
+    strat.__exit__()
     raise_for(rc, e)
     if work is not None:
         work += WorkCounters.from_c(w)
@@ -326,7 +356,8 @@ def adjoint_backward(model: Model, traj: Trajectory, n_chunk: int, loss: LossSpe
 
 def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossSpec | None = None,
                      solver: SolverChoice | None = None, settings: NewtonSettings | None = None,
-                     ctx: Context | None = None, scheme: str = Scheme.backward_euler) -> GradientResult:
+                     ctx: Context | None = None, scheme: str = Scheme.backward_euler,
+                     strategy: str = "analytic") -> GradientResult:
     """adjoint.cpp:299-313; the Frobenius loss runs fully on the device."""
     loss = loss or loss_frobenius()
     settings = settings or NewtonSettings()
@@ -334,12 +365,12 @@ def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossS
     if scheme == Scheme.forward_euler:
         tr = integrate_forward_euler(model, y0, grid, n_chunk, ctx)
         bw = WorkCounters()
-        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx, scheme=scheme)
+        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx, scheme=scheme, strategy=strategy)
         return GradientResult(L, g, tr, bw)
     if not loss.frobenius:
-        tr = integrate_backward_euler(model, y0, grid, n_chunk, settings, solver, ctx)
+        tr = integrate_backward_euler(model, y0, grid, n_chunk, settings, solver, ctx, strategy)
         bw = WorkCounters()
-        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx)
+        L, g = adjoint_backward(model, tr, n_chunk, loss, solver, bw, ctx, strategy=strategy)
         return GradientResult(L, g, tr, bw)
     y0 = _f64(y0)
     if y0.ndim != 2 or y0.shape[1] != model.state_size or y0.shape[0] != grid.n_batch:
@@ -351,9 +382,10 @@ def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossS
     L = C.c_double(0.0)
     wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
     st, sv = settings.c(), solver.c()
-    rc = lib().cko_gradient_adjoint(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
-                                    C.byref(st), C.byref(sv), dptr(states), C.byref(L), dptr(grad), C.byref(wf),
-                                    C.byref(wb), C.byref(e))
+    with _Strategy(ctx, strategy):
+        rc = lib().cko_gradient_adjoint(ctx.h, ctx.model(model), dptr(y0), dptr(grid.times), nb, nt, int(n_chunk),
+                                        C.byref(st), C.byref(sv), dptr(states), C.byref(L), dptr(grad), C.byref(wf),
+                                        C.byref(wb), C.byref(e))
     raise_for(rc, e)
     tr = Trajectory(states, grid, nb, n, WorkCounters.from_c(wf))
     return GradientResult(L.value, grad, tr, WorkCounters.from_c(wb))
@@ -413,16 +445,19 @@ def chunk_residual(model: Model, y_start, dy, t_chunk, dt_chunk, ctx: Context | 
     return out
 
 
-def chunk_jacobian(model: Model, y_start, dy, t_chunk, dt_chunk, ctx: Context | None = None) -> "BlockBidiagonalSystem":
-    """integrate.hpp:57-61 (analytic Jacobian): diag I - J dt, offdiag -I."""
+def chunk_jacobian(model: Model, y_start, dy, t_chunk, dt_chunk, ctx: Context | None = None,
+                   strategy: str = "analytic") -> "BlockBidiagonalSystem":
+    """integrate.hpp:57-61: diag I - J dt, offdiag -I; J by the given JacobianStrategy."""
     y_start, dy, t_chunk, dt_chunk = _chunk_args(model, y_start, dy, t_chunk, dt_chunk)
     ctx = ctx or default_context()
     c, nb, n = dy.shape
     sys = BlockBidiagonalSystem.zeros(c, nb, n)
     e = abi.CkoError()
-    raise_for(lib().cko_chunk_jacobian(ctx.h, ctx.model(model), dptr(y_start), dptr(dy), dptr(t_chunk),
-                                       dptr(dt_chunk), c, nb, dptr(sys.diag), dptr(sys.offdiag) if c > 1 else None,
-                                       C.byref(e)), e)
+    with _Strategy(ctx, strategy):
+        rc = lib().cko_chunk_jacobian(ctx.h, ctx.model(model), dptr(y_start), dptr(dy), dptr(t_chunk),
+                                      dptr(dt_chunk), c, nb, dptr(sys.diag), dptr(sys.offdiag) if c > 1 else None,
+                                      C.byref(e))
+    raise_for(rc, e)
     return sys
 
 

@@ -20,6 +20,7 @@
 
 #include "../../include/chunkode_b200.h"
 #include "cko_kernels.cuh"
+#include "cko_eval.cuh"
 
 using namespace cko;
 
@@ -78,6 +79,7 @@ int state_size(const cko_model_desc* d) {
     case CKO_MODEL_MDS: return d->n_unit >= 1 ? 2 * d->n_unit : -1;
     case CKO_MODEL_CHABOCHE: return d->n_unit >= 1 ? 2 + d->n_unit : -1;
     case CKO_MODEL_NODE: return d->n_unit >= 1 ? d->n_unit : -1;
+    case CKO_MODEL_NEURON: return d->n_unit >= 1 ? 4 * d->n_unit : -1;
   }
   return -1;
 }
@@ -91,6 +93,7 @@ int param_count(const cko_model_desc* d) {
     case CKO_MODEL_MDS: return 3 * u + 1 + nb;
     case CKO_MODEL_CHABOCHE: return 6 + 2 * u + nb + 1;
     case CKO_MODEL_NODE: return W * (u + 1) + W + W * W + W + u * W + u;
+    case CKO_MODEL_NEURON: return 15 * u + nb;
   }
   return -1;
 }
@@ -165,6 +168,7 @@ struct cko_ctx {
   GroupView grp{};
   // kernel timing (cko_ctx_enable_timing)
   int kernel_gen = 2;  // 2: warp-specialised Thomas kernels where instantiated; 1: generic kernels only
+  int jstrat = 0;      // JacobianStrategy of the next calls (cko_ctx_set_jacobian_strategy)
   bool timing = false;
   cudaEvent_t ev[8] = {};
   double last_ms[4] = {0, 0, 0, 0};
@@ -282,6 +286,12 @@ cko_status cko_ctx_set_kernel_generation(cko_ctx* c, int gen) {
 
 int cko_ctx_kernel_generation_used(cko_ctx* c) { return c ? c->last_gen : 0; }
 
+cko_status cko_ctx_set_jacobian_strategy(cko_ctx* c, int strategy) {
+  if (!c || strategy < CKO_JACOBIAN_ANALYTIC || strategy > CKO_JACOBIAN_FINITE_DIFFERENCE) return CKO_ERROR;
+  c->jstrat = strategy;
+  return CKO_OK;
+}
+
 cko_status cko_probe_fp64_tflops(cko_ctx* c, double* tflops, cko_error* err) {
   if (!c || !tflops) return fail(err, CKO_ERROR, "null argument");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -361,8 +371,11 @@ cko_status cko_model_create(cko_ctx* c, const cko_model_desc* d, cko_model** out
   if (!c || !d || !out) return fail(err, CKO_ERROR, "cko_model_create: null argument");
   *out = nullptr;
   const int n = state_size(d);
-  if (n < 1 || d->kind < 0 || d->kind > CKO_MODEL_NODE)
+  if (n < 1 || d->kind < 0 || d->kind > CKO_MODEL_NEURON)
     return fail(err, CKO_STRATEGY_UNAVAILABLE, "model kind %d has no device twin", d->kind);
+  if (d->kind == CKO_MODEL_NEURON && n > kFadMaxN)
+    return fail(err, CKO_STRATEGY_UNAVAILABLE, "neuron model with %d states exceeds the device twin (<= %d)", n,
+                kFadMaxN);
   const bool lane_model = d->kind != CKO_MODEL_SCALAR_DECAY && d->kind != CKO_MODEL_CONSTANT_RATE;
   if (lane_model && d->n_batch_model < 1)
     return fail(err, CKO_SHAPE_MISMATCH, "model needs n_batch_model >= 1");
@@ -478,6 +491,7 @@ constexpr int kThreads = 256;
 cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
                         int nc, const cko_newton_settings* st, const cko_solver_choice* sv, const double* d_dy,
                         cko_work* work, int* iters_out, cko_error* err, const double* d_dts = nullptr) {
+  if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
   if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
   if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
@@ -487,7 +501,8 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   const int n = m->dm.n;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const int gen = d_dts ? 1 : c->kernel_gen;  // explicit step sizes: generic kernels (single-chunk op)
+  // explicit step sizes (single-chunk op) or a non-analytic Jacobian strategy: generic kernels
+  const int gen = (d_dts || c->jstrat != 0) ? 1 : c->kernel_gen;
   const bool nodep = !pcr && gen >= 2 && node_fast_path(m->dm);
   const bool v2 = !nodep && !pcr && gen >= 2 && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const bool p2 = pcr && gen >= 2 && launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
@@ -662,6 +677,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
                         int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* d_dL,
                         double* loss_out, double* grad_out, cko_work* bwd, cko_error* err,
                         bool keep_lambda = false) {
+  if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
   if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
   if (sv->kind == CKO_SOLVER_HYBRID && sv->n_switch < 0)
@@ -671,7 +687,8 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   const int n = m->dm.n, np = m->dm.np;
   const int nc_eff = nc < nt ? nc : nt;
   const bool pcr = sv->kind != CKO_SOLVER_THOMAS;
-  const int gen = keep_lambda ? 1 : c->kernel_gen;  // a carried-in lambda: generic kernels (single-chunk op)
+  // a carried-in lambda (single-chunk op) or a non-analytic Jacobian strategy: generic kernels
+  const int gen = (keep_lambda || c->jstrat != 0) ? 1 : c->kernel_gen;
   const bool nodep = !pcr && gen >= 2 && node_fast_path(m->dm);
   const bool v2 = !nodep && !pcr && gen >= 2 && launch_adjoint_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
   const bool p2 = pcr && gen >= 2 && launch_adjoint_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
@@ -802,6 +819,7 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
 // ---- forward Euler scheme (integrate.cpp:371-407, adjoint.cpp:157-188) ----------------------------
 cko_status fe_forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
                            int nc, cko_work* work, cko_error* err) {
+  if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
   if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
   if (cko_status s = check_lanes(m, nb, err)) return s;
@@ -831,6 +849,7 @@ cko_status fe_forward_core(cko_ctx* c, const cko_model* m, double* d_states, con
 cko_status fe_adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times, int nb,
                            int nt, int nc, int loss_kind, const double* d_dL, double* loss_out, double* grad_out,
                            cko_work* bwd, cko_error* err) {
+  if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
   if (loss_kind == CKO_LOSS_USER && !d_dL) return fail(err, CKO_ERROR, "user loss needs dL");
   if (cko_status s = check_lanes(m, nb, err)) return s;
@@ -1224,6 +1243,7 @@ cko_status cko_newton_solve_chunk(cko_ctx* c, const cko_model* m, const double* 
 static cko_status chunk_op(cko_ctx* c, const cko_model* m, int op, const double* y_start, const double* dy,
                            const double* t_chunk, const double* dt_chunk, int cc, int nb, double* out,
                            double* offdiag_out, cko_error* err) {
+  if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (!c || !m || !y_start || !dy || !t_chunk || !dt_chunk || !out) return fail(err, CKO_ERROR, "null argument");
   if (cc < 1 || nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "chunk op: empty chunk");
   if (cko_status s = check_lanes(m, nb, err)) return s;

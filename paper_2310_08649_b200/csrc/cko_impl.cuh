@@ -22,6 +22,7 @@
 
 #include "cko_kernels.cuh"
 #include "cko_linalg.cuh"
+#include "cko_eval.cuh"
 
 namespace cko {
 
@@ -248,7 +249,7 @@ __device__ unsigned jac_lu_phase(const FwdLaunch& a, const CtaWs& w, int step, i
     const double dt = a.dts ? a.dts[(size_t)(step + k) * nb + b] : t - a.times[(size_t)(step + k) * nb + b];
     SBlk J = w.b(w.lu, p);
     SVec y = w.v(w.yy, p);
-    MD::jacobian(a.m, t, y, J, b);
+    model_jacobian<MD>(a.m, t, y, J, b);
     const double ndt = -dt;
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) J(i, j) = xmul(ndt, J(i, j));
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kMaxThreads) adj_kernel(AdjLaunch a) {
       const double t = a.times[(size_t)m * nb + b];
       const double dt = t - a.times[(size_t)(m - 1) * nb + b];
       SBlk J = w.b(w.lu, p);
-      MD::jacobian(a.m, t, y, J, b);
+      model_jacobian<MD>(a.m, t, y, J, b);
       SVec rhs = w.v(w.hr, p);
       if (a.dL) {
         const double* g = a.dL + (size_t)m * row + (size_t)b * n;
@@ -431,6 +432,9 @@ __host__ __device__ inline void lane_segment(const DevModel& m, int& lo, int& hi
     hi = lo + m.nbm;
   } else if (m.kind == 4) {  // Chaboche: eps_a_b
     lo = 6 + 2 * m.nu;
+    hi = lo + m.nbm;
+  } else if (m.kind == 6) {  // Neuron: I_a per lane
+    lo = 14 * m.nu;
     hi = lo + m.nbm;
   } else {
     lo = hi = m.np;
@@ -520,7 +524,7 @@ __global__ void chunk_op_kernel(DevModel m, int op, const double* __restrict__ y
         h[i] = k == 0 ? xsub(d[i], xmul(h[i], dtv)) : xsub(xsub(d[i], d[i - (ptrdiff_t)nb * n]), xmul(h[i], dtv));
     } else {
       PBlk J{out + (size_t)p * n * n, n};
-      MD::jacobian(m, t[p], yy, J, b);
+      model_jacobian<MD>(m, t[p], yy, J, b);
       for (int e = 0; e < n * n; ++e) fin &= isfinite(J.p[e]);
       for (int e = 0; e < n * n; ++e) J.p[e] = xmul(-dtv, J.p[e]);
       for (int i = 0; i < n; ++i) J(i, i) = xadd(J(i, i), 1.0);
@@ -587,7 +591,7 @@ __global__ void fe_adjoint_kernel(DevModel m, const double* states, const double
       double* w = wq + (size_t)ms * row + (size_t)b * n;
       for (int i = 0; i < n; ++i) w[i] = xmul(lam[i], dt);
       PBlk J{Jb, n};
-      MD::jacobian(m, t0, CVec{states + (size_t)(ms - 1) * row + (size_t)b * n}, J, b);
+      model_jacobian<MD>(m, t0, CVec{states + (size_t)(ms - 1) * row + (size_t)b * n}, J, b);
       for (int e = 0; e < n * n; ++e) fin &= isfinite(Jb[e]);
       for (int i = 0; i < n; ++i) tp[i] = 0.0;
       for (int j = 0; j < n; ++j) {

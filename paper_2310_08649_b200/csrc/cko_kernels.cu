@@ -21,12 +21,14 @@ CKO_DECLARE(lin3)
 CKO_DECLARE(mds)
 CKO_DECLARE(chaboche)
 CKO_DECLARE(node)
+CKO_DECLARE(neuron)
 CKO_V2_DECLARE(scalar)
 CKO_V2_DECLARE(constant)
 CKO_V2_DECLARE(lin3)
 CKO_V2_DECLARE(mds)
 CKO_V2_DECLARE(chaboche)
 CKO_V2_DECLARE(node)
+CKO_V2_DECLARE(neuron)
 
 size_t slab_doubles_per_point(int n, bool pcr) {
   return 2 * (size_t)n + (size_t)n * n + 1 + (pcr ? 3 * (size_t)n * n + n : 0);
@@ -174,6 +176,7 @@ size_t vjp_scratch_doubles(const DevModel& m, int nb, int nt) {
     case 3: return CALL(mds);             \
     case 4: return CALL(chaboche);        \
     case 5: return CALL(node);            \
+    case 6: return CALL(neuron);          \
   }                                       \
   return cudaErrorInvalidValue;
 
@@ -229,7 +232,7 @@ cudaError_t launch_adjoint_pcr2(int kind, int n, const AdjLaunch* a, cudaStream_
 // Load every kernel of the library on the current device (see cko::preload).
 cudaError_t preload_kernels() {
 #define CALL(N) preload_##N()
-  for (int kind = 0; kind <= 5; ++kind) {
+  for (int kind = 0; kind <= 6; ++kind) {
     cudaError_t e = [&]() -> cudaError_t { CKO_SWITCH(kind, CALL) }();
     if (e != cudaSuccess) return e;
     for (int n = 1; n <= 32; ++n) {  // the specialised kernels' probes load them (NotSupported: none for n)

@@ -25,6 +25,7 @@ struct DevModel {
   int np;   // parameter count
   const double* p;        // device parameters
   const double* periods;  // device per-lane periods (LIN3 / NODE), length nbm
+  int jstrat;             // JacobianStrategy of the call: 0 analytic, 1 forward_ad, 2 finite_difference
 };
 
 __device__ __forceinline__ double sign_of(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }

@@ -64,6 +64,7 @@ _NAMES = {
     abi.CKO_MODEL_MDS: "mds",
     abi.CKO_MODEL_CHABOCHE: "chaboche",
     abi.CKO_MODEL_NODE: "node",
+    abi.CKO_MODEL_NEURON: "neuron",
 }
 
 
@@ -94,11 +95,12 @@ class Model:
             abi.CKO_MODEL_MDS: 2 * self.n_unit,
             abi.CKO_MODEL_CHABOCHE: 2 + self.n_unit,
             abi.CKO_MODEL_NODE: self.n_unit,
+            abi.CKO_MODEL_NEURON: 4 * self.n_unit,
         }[self.kind]
 
     @property
     def default_t_max(self) -> float:
-        return 10.0 if self.kind == abi.CKO_MODEL_CHABOCHE else 1.0
+        return 10.0 if self.kind in (abi.CKO_MODEL_CHABOCHE, abi.CKO_MODEL_NEURON) else 1.0
 
     def with_params(self, p) -> "Model":
         """OdeModel::with_params (ode_model.hpp:112-117): count must not change."""
@@ -174,6 +176,18 @@ def build_node_wide(n: int, width: int, n_batch: int, seed: int = 7) -> Model:
     return Model(abi.CKO_MODEL_NODE, p, n_unit=n, width=width, n_batch=n_batch)
 
 
+def build_neuron(n_unit: int, n_batch: int, period: float | None = None) -> Model:
+    """models_neuron.cpp:110-148: fourteen per-unit segments (linspace rules), I_a = linspace(0.1, 1, nb),
+    then the per-unit drive periods T = linspace(0.5, 2, u) (or a constant override)."""
+    if n_unit < 1 or n_batch < 1:
+        raise ShapeMismatch("build_neuron: n_unit, n_batch >= 1")
+    u = n_unit
+    seg = [(0.1, 1.0)] * 8 + [(0.5, 5.0), (0.1, 1.0), (1.5, 15.0), (0.1, 1.0), (1.0, 10.0), (1e-3, 1e-2)]
+    parts = [linspace(lo, hi, u) for lo, hi in seg] + [linspace(0.1, 1.0, n_batch)]
+    parts.append(np.full(u, float(period)) if period is not None else linspace(0.5, 2.0, u))
+    return Model(abi.CKO_MODEL_NEURON, np.concatenate(parts), n_unit=u, n_batch=n_batch)
+
+
 def build_lin3(n_batch: int) -> Model:
     """A = [[-1,.5,0],[.5,-1e3,10],[0,10,-1e6]], f_a = 1, T_b = linspace(1e-2,1,nb)."""
     p = np.array([-1.0, 0.5, 0.0, 0.5, -1e3, 10.0, 0.0, 10.0, -1e6, 1.0], dtype=np.float64)
@@ -190,6 +204,8 @@ def build_problem(key: str, n_unit: int, n_batch: int, seed: int = 7) -> Model:
         return build_neural_ode(n_unit, n_batch, seed)
     if key == "lin3":
         return build_lin3(n_batch)
+    if key == "neuron":
+        return build_neuron(n_unit, n_batch)
     from .errors import Error
     raise Error(f"unknown problem '{key}' (expected mds, chaboche, node, or lin3)")
 
@@ -203,4 +219,5 @@ def param_count(kind: int, n_unit: int = 0, width: int = 0, n_batch: int = 0) ->
         abi.CKO_MODEL_MDS: 3 * u + 1 + nb,
         abi.CKO_MODEL_CHABOCHE: 6 + 2 * u + nb + 1,
         abi.CKO_MODEL_NODE: W * (u + 1) + W + W * W + W + u * W + u,
+        abi.CKO_MODEL_NEURON: 15 * u + nb,
     }[kind]
