@@ -14,10 +14,10 @@ src/bench.cpp:16-443, so GPU rows line up with the reference's rows:
   gradient_fd_oracle             the central-difference reference gradient
                                  (adjoint.cpp:315-342), on the device integrator
 
-Every trial runs on the GPU through the C ABI (api.py). Timings are wall-clock
-around the synchronous calls, as the reference's steady_clock timers
-(bench.cpp:87-111). Jacobian strategies other than `analytic` have no device
-twin and report StrategyUnavailable in the status column.
+Every trial runs on the GPU through the C ABI (api.py), with the trial's
+Jacobian strategy (analytic, forward_ad, finite_difference). Timings are
+wall-clock around the synchronous calls, as the reference's steady_clock
+timers (bench.cpp:87-111).
 """
 from __future__ import annotations
 
@@ -31,7 +31,7 @@ from typing import Iterable
 import numpy as np
 
 from . import api
-from .errors import Error, SizeGuardExceeded, StrategyUnavailable
+from .errors import Error, SizeGuardExceeded
 from .models import build_problem
 
 CSV_HEADER = ("problem,n_unit,n_size,n_batch,n_time,n_chunk,jacobian,gradient,solver,integration,repeat,"
@@ -130,8 +130,6 @@ def validate_trial_config(cfg: TrialConfig) -> None:
 
 
 def _model(cfg: TrialConfig):
-    if cfg.problem == "neuron":
-        raise StrategyUnavailable("model 'neuron' has no device twin")
     return build_problem(cfg.problem, cfg.n_unit, cfg.n_batch, cfg.seed)
 
 
@@ -161,20 +159,20 @@ def gradient_fd_oracle(model, y0, grid: api.TimeGrid, loss: api.LossSpec | None 
 
 def _run_once(model, cfg: TrialConfig, grid: api.TimeGrid, ctx):
     """bench.cpp:79-118."""
-    if cfg.jacobian != "analytic":
-        raise StrategyUnavailable(f"jacobian strategy '{cfg.jacobian}' has no device path (analytic only)")
     nb, ns = cfg.n_batch, model.state_size
     solver, scheme = _solver(cfg), _scheme(cfg)
     y0 = np.zeros((nb, ns))  # every bundled problem starts from rest
     t0 = time.perf_counter()
-    traj = (api.integrate_backward_euler(model, y0, grid, cfg.n_chunk, api.NewtonSettings(), solver, ctx)
+    traj = (api.integrate_backward_euler(model, y0, grid, cfg.n_chunk, api.NewtonSettings(), solver, ctx,
+                                         strategy=cfg.jacobian)
             if scheme == api.Scheme.backward_euler else api.integrate_forward_euler(model, y0, grid, cfg.n_chunk, ctx))
     fwd = time.perf_counter() - t0
     loss = api.loss_frobenius()
     bwd, L, gn = 0.0, float("nan"), 0.0
     if cfg.gradient == "adjoint":
         t0 = time.perf_counter()
-        L, g = api.adjoint_backward(model, traj, cfg.n_chunk, loss, solver, None, ctx, scheme=scheme)
+        L, g = api.adjoint_backward(model, traj, cfg.n_chunk, loss, solver, None, ctx, scheme=scheme,
+                                    strategy=cfg.jacobian)
         bwd = time.perf_counter() - t0
         gn = math.sqrt(float(np.sum(g * g)))
     elif cfg.gradient == "fd_oracle":
@@ -354,13 +352,12 @@ def dump_trajectory(cfg: TrialConfig, os_, ctx=None) -> None:
     """bench.cpp:418-441: one integration, `time,batch,component,value` per (step, lane, component)."""
     validate_trial_config(cfg)
     model = _model(cfg)
-    if cfg.jacobian != "analytic":
-        raise StrategyUnavailable(f"jacobian strategy '{cfg.jacobian}' has no device path (analytic only)")
     ns = model.state_size
     t_max = cfg.t_max if cfg.t_max > 0.0 else DEFAULT_T_MAX[cfg.problem]
     grid = api.TimeGrid.uniform(cfg.n_time, cfg.n_batch, t_max)
     y0 = np.zeros((cfg.n_batch, ns))
-    traj = (api.integrate_backward_euler(model, y0, grid, cfg.n_chunk, api.NewtonSettings(), _solver(cfg), ctx)
+    traj = (api.integrate_backward_euler(model, y0, grid, cfg.n_chunk, api.NewtonSettings(), _solver(cfg), ctx,
+                                         strategy=cfg.jacobian)
             if _scheme(cfg) == api.Scheme.backward_euler
             else api.integrate_forward_euler(model, y0, grid, cfg.n_chunk, ctx))
     os_.write("time,batch,component,value\n")

@@ -11,8 +11,8 @@
 //  * a model crosses the ABI as cko_model_desc: its kind from name(), its sizes
 //    from state_size() / params().size() / n_batch() (no extra arguments);
 //    models without a device twin throw StrategyUnavailable — no CPU fallback;
-//  * JacobianStrategy: the device evaluates analytic Jacobians; other
-//    strategies throw StrategyUnavailable;
+//  * JacobianStrategy: analytic, forward_ad (device dual numbers) and
+//    finite_difference are all honoured on the device;
 //  * Scheme: backward_euler and forward_euler both run on the device;
 //  * LossSpec: loss_frobenius() (defined here) runs fused on the device; any
 //    other LossSpec is evaluated through its callbacks and its state gradient
@@ -101,6 +101,10 @@ struct DeviceModel {
       d.kind = CKO_MODEL_CHABOCHE;
       d.n_unit = n - 2;
       d.n_batch_model = np - 6 - 2 * d.n_unit - 1;
+    } else if (name == "neuron") {  // [14 per-unit segments, I_a(nb), T(u)]
+      d.kind = CKO_MODEL_NEURON;
+      d.n_unit = n / 4;
+      d.n_batch_model = np - 15 * d.n_unit;
     } else if (name == "node" || name == "node_wide") {
       // np = W (n+1) + W + W^2 + W + n W + n  ->  W^2 + (2n + 3) W + n - np = 0
       d.kind = CKO_MODEL_NODE;
@@ -120,9 +124,13 @@ struct DeviceModel {
   DeviceModel& operator=(const DeviceModel&) = delete;
 };
 
-void require_analytic(JacobianStrategy s) {
-  if (s != JacobianStrategy::analytic)
-    throw StrategyUnavailable("the B200 path evaluates analytic Jacobians only");
+// The call's JacobianStrategy on the device context (analytic, forward-mode duals or central differences,
+// ode_model.hpp:14); every entry point sets it, so one context serves calls with different strategies.
+void use_strategy(JacobianStrategy s) {
+  const int k = s == JacobianStrategy::forward_ad          ? CKO_JACOBIAN_FORWARD_AD
+                : s == JacobianStrategy::finite_difference ? CKO_JACOBIAN_FINITE_DIFFERENCE
+                                                           : CKO_JACOBIAN_ANALYTIC;
+  cko_ctx_set_jacobian_strategy(ctx(), k);
 }
 
 cko_solver_choice solver_c(const SolverChoice& s) {
@@ -208,7 +216,7 @@ Trajectory integrate_backward_euler(const OdeModel& model, const Array2d& y0, co
                                     const NewtonSettings& settings, const SolverChoice& solver,
                                     JacobianStrategy strategy) {
   check_integrate(model, y0, grid, n_chunk);
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   const int nb = y0.rows(), ns = y0.cols();
   Trajectory tr = make_traj(grid, nb, ns);
@@ -268,7 +276,7 @@ void chunk_jacobian(const OdeModel& model, const Array2d& y_start, const Batched
   check_chunk(model, y_start, dy, t_chunk, dt_chunk);
   require(out.n_chunk() == dy.n_chunk() && out.n_batch() == dy.n_batch() && out.n_size() == dy.n_size(),
           "chunk_jacobian: out system shape must match dy");
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   cko_error e{};
   check(cko_chunk_jacobian(ctx(), dm.m, y_start.data(), dy.data(), t_chunk.data(), dt_chunk.data(), dy.n_chunk(),
@@ -281,7 +289,7 @@ int newton_solve_chunk(const OdeModel& model, const Array2d& y_start, BatchedChu
                        const SolverChoice& solver, JacobianStrategy strategy, WorkCounters* work,
                        int chunk_start_step) {
   check_chunk(model, y_start, dy, t_chunk, dt_chunk);
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   cko_newton_settings st{settings.tol_a, settings.tol_r, settings.max_iter};
   cko_solver_choice sv = solver_c(solver);
@@ -303,7 +311,7 @@ std::pair<double, std::vector<double>> adjoint_backward(const OdeModel& model, c
   check_loss(loss);
   require(traj.n_size == model.state_size(), "adjoint: trajectory width != model size");
   require(n_chunk >= 1, "adjoint: n_chunk must be >= 1");
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   const bool fused = is_frobenius(loss);
   double L = 0.0;
@@ -339,7 +347,7 @@ GradientResult gradient_adjoint(const OdeModel& model, const Array2d& y0, const 
   GradientResult res;
   if (scheme == Scheme::backward_euler && is_frobenius(loss)) {  // one upload, the trajectory stays resident
     check_integrate(model, y0, grid, n_chunk);
-    require_analytic(strategy);
+    use_strategy(strategy);
     DeviceModel dm(model);
     const int nb = y0.rows(), ns = y0.cols();
     res.trajectory = make_traj(grid, nb, ns);
@@ -381,7 +389,7 @@ void adjoint_step_sequential(const OdeModel& model, const Array2d& y_i, const Ar
   require(int(t_i.size()) == nb && int(t_prev.size()) == nb, "adjoint step: time spans");
   require(dL_dy_i.rows() == nb && dL_dy_i.cols() == ns, "adjoint step: loss jump shape");
   check_state(model, state, nb);
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   cko_solver_choice sv = solver_c(solver);
   cko_error e{};
@@ -399,7 +407,7 @@ void adjoint_chunk_solve(const OdeModel& model, const Trajectory& traj, int step
   require(dL_dy.rows() == traj.states.rows() && dL_dy.cols() == traj.states.cols(),
           "adjoint chunk: dL_dy must be shaped like the trajectory states");
   check_state(model, state, traj.n_batch);
-  require_analytic(strategy);
+  use_strategy(strategy);
   DeviceModel dm(model);
   cko_solver_choice sv = solver_c(solver);
   cko_work w{};

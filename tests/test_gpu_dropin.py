@@ -1,6 +1,6 @@
 """The C++ drop-in (paper_2310_08649_b200/shim): the reference's own C++ API, unchanged signatures,
 served by the B200 path. tests/cpp/acceptance_b200 replays the reference's release gate
-(acceptance.cpp criteria 1-5, 7, 8) through it; every integrate / adjoint / solve call runs on the GPU."""
+(acceptance.cpp criteria 1-5, 7, 8, plus the strategies through the device chunk_jacobian) through it; every integrate / adjoint / solve call runs on the GPU."""
 import os
 import subprocess
 
@@ -37,4 +37,4 @@ def test_reference_acceptance_gate_through_the_dropin():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 7
+    assert r.stdout.count("PASS") == 8
