@@ -572,16 +572,43 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
     CUDA_TRY(c->pin.ensure(64));
     std::memset(info, 0, sizeof info);
     c->iters_host.assign(n_chunks, 0);
-    c->mark(0);
-    CUDA_TRY(node_forward(m->dm, d_states, d_times, d_dy, nb, nt, nc, st->tol_a, st->tol_r, st->max_iter,
-                          c->scratch.as<double>(), c->r0.as<double>(), c->rn.as<double>(), c->status.as<unsigned>(),
-                          c->pin.as<unsigned>(0), c->key.as<unsigned long long>(), c->grp, c->gs.as<GridSync>(),
-                          c->iters_host.data(), info, c->stream));
-    c->mark(1);
-    CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
-                             c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    key = *c->pin.as<unsigned long long>(16);
+    static const bool host_loop = [] {
+      const char* v = std::getenv("CKO_NODE_HOST_LOOP");  // A/B: the host-driven Newton loop
+      return v && v[0] == '1';
+    }();
+    if (host_loop) {
+      c->mark(0);
+      CUDA_TRY(node_forward(m->dm, d_states, d_times, d_dy, nb, nt, nc, st->tol_a, st->tol_r, st->max_iter,
+                            c->scratch.as<double>(), c->r0.as<double>(), c->rn.as<double>(), c->status.as<unsigned>(),
+                            c->pin.as<unsigned>(0), c->key.as<unsigned long long>(), c->grp, c->gs.as<GridSync>(),
+                            c->iters_host.data(), info, c->stream));
+      c->mark(1);
+      CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      key = *c->pin.as<unsigned long long>(16);
+    } else {  // the Newton loop on the device: one graph launch for the whole integration
+      CUDA_TRY(c->iters.ensure(sizeof(int) * (16 + (size_t)n_chunks)));
+      CUDA_TRY(c->pin.ensure(64 + sizeof(int) * (16 + (size_t)n_chunks)));
+      c->mark(0);
+      CUDA_TRY(node_forward_graph(m->dm, d_states, d_times, d_dy, nb, nt, nc, st->tol_a, st->tol_r, st->max_iter,
+                                  c->scratch.as<double>(), c->r0.as<double>(), c->rn.as<double>(),
+                                  c->status.as<unsigned>(), c->key.as<unsigned long long>(), c->grp,
+                                  c->gs.as<GridSync>(), c->iters.as<int>(), c->stream));
+      c->mark(1);
+      CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(64), c->iters.p, sizeof(int) * (16 + (size_t)n_chunks),
+                               cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      key = *c->pin.as<unsigned long long>(16);
+      const int* ctl = c->pin.as<int>(64);
+      info[0] = ctl[2];
+      info[1] = ctl[5];
+      info[2] = ctl[6];
+      info[3] = ctl[4];
+      c->iters_host.assign(ctl + 16, ctl + 16 + n_chunks);
+    }
     c->last_launches = 1 + 6 * (int)n_chunks;
     c->last_gen = 2;
   } else {

@@ -91,6 +91,12 @@ cudaError_t launch_adjoint_v2(int kind, int n, const AdjLaunch* a, cudaStream_t 
 // Newton loop (cko_node.cu). Scratch: node_scratch_doubles(nb, min(nc, nt)).
 bool node_fast_path(const DevModel& m);
 size_t node_scratch_doubles(int nb, int c);
+// The same integration with the Newton loop on the device (nested CUDA-graph WHILE nodes); d_ctl holds
+// 16 control ints then the per-chunk iteration counts.
+cudaError_t node_forward_graph(const DevModel& m, double* states, const double* times, const double* dy, int nb,
+                               int nt, int nc, double tol_a, double tol_r, int max_iter, double* scratch, double* r0,
+                               double* rn, unsigned* d_flags, unsigned long long* sing_key, const GroupView& grp,
+                               GridSync* gs, int* d_ctl, cudaStream_t st);
 cudaError_t node_forward(const DevModel& m, double* states, const double* times, const double* dy, int nb, int nt,
                          int nc, double tol_a, double tol_r, int max_iter, double* scratch, double* r0, double* rn,
                          unsigned* d_flags, unsigned* h_flags, unsigned long long* sing_key, const GroupView& grp,

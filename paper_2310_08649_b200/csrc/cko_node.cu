@@ -19,6 +19,8 @@
 // follows the reference; the products accumulate in tensor-core order.
 #include <cmath>
 #include <cstring>
+#include <utility>
+#include <vector>
 
 #include "cko_kernels.cuh"
 #include "cko_lu_thread.cuh"
@@ -59,7 +61,13 @@ constexpr int kEvalSmem = (W * BC + TP * W0 + TP * N) * 8;  // operand / product
 // descending rows of a reversed adjoint chunk).
 __global__ void __launch_bounds__(kEvalThreads) node_eval_kernel(DevModel m, const double* states,
                                                                  const double* times, int row0, int dir, int nb,
-                                                                 int P, double* H, double* J, int want_j) {
+                                                                 int P, double* H, double* J, int want_j,
+                                                                 const int* dyn) {
+  if (dyn) {  // device-driven Newton loop: the chunk comes from the control block
+    if (dyn[2]) return;
+    row0 = dyn[0] + 1;
+    P = dyn[1] * nb;
+  }
   extern __shared__ __align__(16) double smem[];
   double* sB = smem;               // operand  (W x 72) = 72 KB
   double* sX = sB;                 // products overwrite it after the tensor-core pass
@@ -156,7 +164,11 @@ __global__ void __launch_bounds__(kEvalThreads) node_eval_kernel(DevModel m, con
 // Residual of the chunk's points + lane norms + predicate flags (integrate.cpp:64-95, 176-188).
 __global__ void node_residual_kernel(const double* states, const double* times, const double* H, int step, int c,
                                      int nb, double* R, double* r0, double* rn, int first, double tol_a,
-                                     double tol_r, unsigned* flags) {
+                                     double tol_r, unsigned* flags, const int* dyn) {
+  if (dyn) {
+    if (dyn[2]) return;
+    step = dyn[0], c = dyn[1];
+  }
   const size_t row = (size_t)nb * N;
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     double acc = 0.0;
@@ -194,7 +206,11 @@ __global__ void node_residual_kernel(const double* states, const double* times, 
 __global__ void __launch_bounds__(128) node_residual_pp_kernel(const double* states, const double* times,
                                                                const double* H, int step, int c, int nb, double* R,
                                                                double* r0, double* rn, int first, double tol_a,
-                                                               double tol_r, unsigned* flags) {
+                                                               double tol_r, unsigned* flags, const int* dyn) {
+  if (dyn) {
+    if (dyn[2]) return;
+    step = dyn[0], c = dyn[1];
+  }
   __shared__ double ps[128];
   const size_t row = (size_t)nb * N;
   const int Lb = 128 / c, b0 = blockIdx.x * Lb;
@@ -240,7 +256,11 @@ constexpr int kRec = N * N + N + 6;  // LU | 1/U_ii | perm (N + 1 ints) — 16-b
 // dL + dt J^T lambda) and factor it (lu_factor_block rule).
 __global__ void node_factor_kernel(const double* J, const double* times, int step_or_hi, int c, int nb,
                                    int adjoint, double* recs, unsigned long long* sing_key, unsigned long long ord,
-                                   int nc, unsigned* flags) {
+                                   int nc, unsigned* flags, const int* dyn) {
+  if (dyn) {
+    if (dyn[2]) return;
+    step_or_hi = dyn[0], c = dyn[1];
+  }
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c * nb; p += gridDim.x * blockDim.x) {
     const int k = p / nb, b = p % nb;
     const int m = adjoint ? step_or_hi - k : step_or_hi + 1 + k;
@@ -368,7 +388,12 @@ __device__ __forceinline__ void sub_wait() { asm volatile("cp.async.wait_group %
 
 // Thread per lane: forward substitution x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k.
 __global__ void __launch_bounds__(kSubThreads) node_thomas_fwd_kernel(double* states, const double* R,
-                                                                      const double* recs, int step, int c, int nb) {
+                                                                      const double* recs, int step, int c, int nb,
+                                                                      const int* dyn) {
+  if (dyn) {
+    if (dyn[2]) return;
+    step = dyn[0], c = dyn[1];
+  }
   extern __shared__ __align__(16) double sub_smem[];
   double* my = sub_smem + (size_t)threadIdx.x * kSubD * kSubS;
   const size_t row = (size_t)nb * N;
@@ -452,7 +477,11 @@ __global__ void __launch_bounds__(kSubThreads) node_thomas_adj_kernel(const doub
   }
 }
 
-__global__ void node_init_chunk_kernel(double* states, const double* dy, int step, int c, int nb) {
+__global__ void node_init_chunk_kernel(double* states, const double* dy, int step, int c, int nb, const int* dyn) {
+  if (dyn) {
+    if (dyn[2]) return;
+    step = dyn[0], c = dyn[1];
+  }
   const size_t row = (size_t)nb * N;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < (size_t)c * row;
        e += (size_t)gridDim.x * blockDim.x) {
@@ -465,7 +494,9 @@ __global__ void node_init_chunk_kernel(double* states, const double* dy, int ste
 
 // One-thread exchange of the predicate flags with the group (same generation
 // counter as the grid barriers).
-__global__ void node_group_flags_kernel(GroupView g, GridSync* gs, unsigned* flags, uint64_t budget_ns) {
+__global__ void node_group_flags_kernel(GroupView g, GridSync* gs, unsigned* flags, uint64_t budget_ns,
+                                        const int* dyn) {
+  if (dyn && dyn[2]) return;
   if (threadIdx.x == 0 && g.world > 1) {
     gs->ext_gen += 1;
     *flags = group_exchange(g, gs->ext_gen, *flags, globaltimer_ns() + budget_ns);
@@ -622,16 +653,6 @@ cudaError_t launch_node_vectors_dmma(const DevModel& m, const double* states, co
   return cudaGetLastError();
 }
 
-cudaError_t preload_node_kernels() {
-  using namespace node;
-  for (const void* f : {(const void*)node_eval_kernel, (const void*)node_residual_kernel,
-                        (const void*)node_residual_pp_kernel, (const void*)node_factor_kernel,
-                        (const void*)node_thomas_fwd_kernel, (const void*)node_adj_rhs_kernel,
-                        (const void*)node_thomas_adj_kernel, (const void*)node_init_chunk_kernel,
-                        (const void*)node_group_flags_kernel, (const void*)node_vectors_dmma_kernel})
-    if (cudaError_t e = preload(f)) return e;
-  return cudaSuccess;
-}
 
 bool node_fast_path(const DevModel& m) { return m.kind == 5 && m.n == node::N && m.W == node::W; }
 
@@ -646,7 +667,7 @@ cudaError_t node_eval(const DevModel& m, const double* states, const double* tim
   if (attr != cudaSuccess) return attr;
   const int tiles = (P + node::TP - 1) / node::TP;
   node::node_eval_kernel<<<tiles < 2 * 148 ? tiles : 2 * 148, node::kEvalThreads, node::kEvalSmem, st>>>(
-      m, states, times, row0, dir, nb, P, H, J, want_j ? 1 : 0);
+      m, states, times, row0, dir, nb, P, H, J, want_j ? 1 : 0, nullptr);
   return cudaGetLastError();
 }
 
@@ -657,10 +678,10 @@ static void launch_node_residual(const double* states, const double* times, cons
   if (c <= 128) {
     const int Lb = 128 / c;
     node_residual_pp_kernel<<<(nb + Lb - 1) / Lb, 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, first,
-                                                                tol_a, tol_r, flags);
+                                                                tol_a, tol_r, flags, nullptr);
   } else {
     node_residual_kernel<<<blocks_for(nb, 128), 128, 0, st>>>(states, times, H, step, c, nb, R, r0, rn, first, tol_a,
-                                                             tol_r, flags);
+                                                             tol_r, flags, nullptr);
   }
 }
 
@@ -681,7 +702,7 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
   int step = 0, chunk = 0;
   info[0] = 0;
   auto flags = [&](unsigned& f) -> cudaError_t {
-    if (grp.world > 1) node_group_flags_kernel<<<1, 32, 0, st>>>(grp, gs, d_flags, 60ull * 1000 * 1000 * 1000);
+    if (grp.world > 1) node_group_flags_kernel<<<1, 32, 0, st>>>(grp, gs, d_flags, 60ull * 1000 * 1000 * 1000, nullptr);
     cudaError_t ee = cudaMemcpyAsync(h_flags, d_flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
     if (ee == cudaSuccess) ee = cudaStreamSynchronize(st);
     f = *h_flags;
@@ -690,7 +711,7 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
   while (step < nt) {
     const int c = min(nc, nt - step);
     const int P = c * nb;
-    node_init_chunk_kernel<<<blocks_for((size_t)P * N, 256), 256, 0, st>>>(states, dy, step, c, nb);
+    node_init_chunk_kernel<<<blocks_for((size_t)P * N, 256), 256, 0, st>>>(states, dy, step, c, nb, nullptr);
     if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     launch_node_residual(states, times, H, step, c, nb, R, r0, rn, 1, tol_a, tol_r, d_flags, st);
@@ -705,10 +726,11 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
       if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
       node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step, c, nb, 0, recs, sing_key, 0, nc,
-                                                               d_flags);
+                                                               d_flags, nullptr);
       const cudaError_t fattr = allow_smem((const void*)node_thomas_fwd_kernel, kSubSmem);
       if (fattr != cudaSuccess) return fattr;
-      node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(states, R, recs, step, c, nb);
+      node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(states, R, recs, step, c, nb,
+                                                                                          nullptr);
       if ((e = node_eval(m, states, times, step + 1, 1, nb, P, H, Jb, false, st)) != cudaSuccess) return e;
       launch_node_residual(states, times, H, step, c, nb, R, r0, rn, 0, tol_a, tol_r, d_flags, st);
       if ((e = flags(f)) != cudaSuccess) return e;
@@ -728,6 +750,208 @@ cudaError_t node_forward(const DevModel& m, double* states, const double* times,
   }
   info[3] = chunk;
   return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Device-driven Newton loop (one CUDA graph per integration): an outer WHILE
+// node walks the chunks, an inner WHILE node runs the Newton iterations; the
+// predicate (integrate.cpp:176-188) and the divergence / singular-block
+// outcomes are decided by one-thread control kernels that set the
+// conditionals on the device, so no iteration waits on a host round trip.
+// The kernels read the chunk (step, c) from the control block and return at
+// once after a failure was recorded (dyn[2] != 0).
+//   dyn: [0] step [1] c [2] status (0 ok, 1 singular, 2 divergence, 4 timeout)
+//        [3] iteration [4] chunk [5] failing chunk's first step [6] its iteration
+//        [7] nt [8] nc [9] max_iter;   iters[chunk] = Newton iterations.
+// ---------------------------------------------------------------------------
+namespace node {
+
+__global__ void ctl_newton_start(int* dyn, const unsigned* flags, cudaGraphConditionalHandle outer,
+                                 cudaGraphConditionalHandle inner) {
+  const unsigned f = *flags;
+  int st = 0;
+  if (f & FLAG_TIMEOUT)
+    st = 4;
+  else if (f & FLAG_NON_FINITE)
+    st = 2, dyn[5] = dyn[0] + 1, dyn[6] = 0;
+  dyn[3] = 0;
+  if (st) {
+    dyn[2] = st;
+    cudaGraphSetConditional(outer, 0);
+  }
+  cudaGraphSetConditional(inner, (!st && (f & FLAG_NOT_CONVERGED)) ? 1u : 0u);
+}
+
+__global__ void ctl_newton_iter(int* dyn, unsigned* flags, cudaGraphConditionalHandle outer,
+                                cudaGraphConditionalHandle inner) {
+  if (dyn[3] == dyn[9]) {  // the iteration cap: NewtonDivergence (integrate.cpp:247-254)
+    dyn[2] = 2, dyn[5] = dyn[0] + 1, dyn[6] = dyn[9];
+    cudaGraphSetConditional(inner, 0);
+    cudaGraphSetConditional(outer, 0);
+    return;
+  }
+  dyn[3] += 1;
+  *flags = 0;
+}
+
+__global__ void ctl_newton_end(int* dyn, const unsigned* flags, const unsigned long long* key,
+                               cudaGraphConditionalHandle outer, cudaGraphConditionalHandle inner) {
+  if (dyn[2]) {
+    cudaGraphSetConditional(inner, 0);
+    cudaGraphSetConditional(outer, 0);
+    return;
+  }
+  const unsigned f = *flags;
+  int st = 0;
+  if (f & FLAG_TIMEOUT)
+    st = 4;
+  else if (*key != ~0ull || (f & FLAG_SINGULAR))  // a singular block here or on a peer rank
+    st = 1;
+  else if (f & FLAG_NON_FINITE)
+    st = 2;
+  if (st) {
+    dyn[2] = st, dyn[5] = dyn[0] + 1, dyn[6] = dyn[3];
+    cudaGraphSetConditional(inner, 0);
+    cudaGraphSetConditional(outer, 0);
+    return;
+  }
+  cudaGraphSetConditional(inner, (f & FLAG_NOT_CONVERGED) ? 1u : 0u);
+}
+
+__global__ void ctl_chunk_end(int* dyn, int* iters, unsigned* flags, cudaGraphConditionalHandle outer) {
+  if (dyn[2]) {
+    cudaGraphSetConditional(outer, 0);
+    return;
+  }
+  iters[dyn[4]] = dyn[3];
+  dyn[0] += dyn[1];
+  dyn[4] += 1;
+  const int rem = dyn[7] - dyn[0];
+  dyn[1] = rem < dyn[8] ? rem : dyn[8];
+  *flags = 0;
+  cudaGraphSetConditional(outer, dyn[0] < dyn[7] ? 1u : 0u);
+}
+
+// The last node of a captured chain (the one nothing depends on).
+cudaError_t graph_leaf(cudaGraph_t g, cudaGraphNode_t* leaf) {
+  size_t n = 0;
+  cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+  if (e != cudaSuccess) return e;
+  std::vector<cudaGraphNode_t> nodes(n);
+  if ((e = cudaGraphGetNodes(g, nodes.data(), &n)) != cudaSuccess) return e;
+  for (cudaGraphNode_t v : nodes) {
+    size_t k = 0;
+    if ((e = cudaGraphNodeGetDependentNodes(v, nullptr, &k)) != cudaSuccess) return e;
+    if (k == 0) {
+      *leaf = v;
+      return cudaSuccess;
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace node
+
+cudaError_t node_forward_graph(const DevModel& m, double* states, const double* times, const double* dy, int nb,
+                               int nt, int nc, double tol_a, double tol_r, int max_iter, double* scratch, double* r0,
+                               double* rn, unsigned* d_flags, unsigned long long* sing_key, const GroupView& grp,
+                               GridSync* gs, int* d_ctl, cudaStream_t st) {
+  using namespace node;
+  const int cmax = nc < nt ? nc : nt;
+  const size_t Pmax = (size_t)cmax * nb;
+  double* H = scratch;
+  double* Jb = H + Pmax * N;
+  double* R = Jb + Pmax * N * N;
+  double* recs = R + Pmax * N;
+  int* dyn = d_ctl;
+  int* iters = d_ctl + 16;
+  cudaError_t e;
+  const int host_ctl[10] = {0, cmax, 0, 0, 0, 0, 0, nt, nc, max_iter};
+  if ((e = cudaMemcpyAsync(dyn, host_ctl, sizeof host_ctl, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(d_flags, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  for (const auto& [f, b] : {std::pair<const void*, int>{(const void*)node_eval_kernel, kEvalSmem},
+                             {(const void*)node_thomas_fwd_kernel, kSubSmem}})
+    if ((e = allow_smem(f, b)) != cudaSuccess) return e;
+  const int eval_grid = (int)((Pmax + TP - 1) / TP) < 2 * 148 ? (int)((Pmax + TP - 1) / TP) : 2 * 148;
+  const int Lb = cmax <= 128 ? 128 / cmax : 0;
+  cudaStream_t cs;
+  if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  cudaGraph_t g = nullptr, outer_body = nullptr, inner_body = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  auto eval = [&](int want_j) {
+    node_eval_kernel<<<eval_grid, kEvalThreads, kEvalSmem, cs>>>(m, states, times, 0, 1, nb, (int)Pmax, H, Jb, want_j,
+                                                               dyn);
+  };
+  auto residual = [&](int first) {
+    if (Lb)
+      node_residual_pp_kernel<<<(nb + Lb - 1) / Lb, 128, 0, cs>>>(states, times, H, 0, cmax, nb, R, r0, rn, first, tol_a,
+                                                                 tol_r, d_flags, dyn);
+    else
+      node_residual_kernel<<<blocks_for(nb, 128), 128, 0, cs>>>(states, times, H, 0, cmax, nb, R, r0, rn, first, tol_a,
+                                                               tol_r, d_flags, dyn);
+    if (grp.world > 1) node_group_flags_kernel<<<1, 32, 0, cs>>>(grp, gs, d_flags, 60ull * 1000 * 1000 * 1000, dyn);
+  };
+  auto build = [&]() -> cudaError_t {
+    cudaError_t r;
+    if ((r = cudaGraphCreate(&g, 0)) != cudaSuccess) return r;
+    cudaGraphConditionalHandle h_outer, h_inner;
+    if ((r = cudaGraphConditionalHandleCreate(&h_outer, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return r;
+    cudaGraphNodeParams op = {};
+    op.type = cudaGraphNodeTypeConditional;
+    op.conditional.handle = h_outer;
+    op.conditional.type = cudaGraphCondTypeWhile;
+    op.conditional.size = 1;
+    cudaGraphNode_t outer_node;
+    if ((r = cudaGraphAddNode(&outer_node, g, nullptr, 0, &op)) != cudaSuccess) return r;
+    outer_body = op.conditional.phGraph_out[0];
+    if ((r = cudaGraphConditionalHandleCreate(&h_inner, outer_body, 0, 0)) != cudaSuccess) return r;
+    // chunk prologue: initial iterate, rate, first residual and the predicate
+    if ((r = cudaStreamBeginCaptureToGraph(cs, outer_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) !=
+        cudaSuccess)
+      return r;
+    node_init_chunk_kernel<<<blocks_for(Pmax * N, 256), 256, 0, cs>>>(states, dy, 0, cmax, nb, dyn);
+    eval(0);
+    residual(1);
+    ctl_newton_start<<<1, 1, 0, cs>>>(dyn, d_flags, h_outer, h_inner);
+    if ((r = cudaStreamEndCapture(cs, &outer_body)) != cudaSuccess) return r;
+    cudaGraphNode_t pro_leaf;
+    if ((r = graph_leaf(outer_body, &pro_leaf)) != cudaSuccess) return r;
+    // Newton iterations
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_inner;
+    ip.conditional.type = cudaGraphCondTypeWhile;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inner_node;
+    if ((r = cudaGraphAddNode(&inner_node, outer_body, &pro_leaf, 1, &ip)) != cudaSuccess) return r;
+    inner_body = ip.conditional.phGraph_out[0];
+    if ((r = cudaStreamBeginCaptureToGraph(cs, inner_body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed)) !=
+        cudaSuccess)
+      return r;
+    ctl_newton_iter<<<1, 1, 0, cs>>>(dyn, d_flags, h_outer, h_inner);
+    eval(1);
+    node_factor_kernel<<<blocks_for(Pmax, 128), 128, 0, cs>>>(Jb, times, 0, cmax, nb, 0, recs, sing_key, 0, nc, d_flags,
+                                                             dyn);
+    node_thomas_fwd_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, cs>>>(states, R, recs, 0, cmax, nb,
+                                                                                        dyn);
+    eval(0);
+    residual(0);
+    ctl_newton_end<<<1, 1, 0, cs>>>(dyn, d_flags, sing_key, h_outer, h_inner);
+    if ((r = cudaStreamEndCapture(cs, &inner_body)) != cudaSuccess) return r;
+    // chunk epilogue
+    if ((r = cudaStreamBeginCaptureToGraph(cs, outer_body, &inner_node, nullptr, 1, cudaStreamCaptureModeRelaxed)) !=
+        cudaSuccess)
+      return r;
+    ctl_chunk_end<<<1, 1, 0, cs>>>(dyn, iters, d_flags, h_outer);
+    if ((r = cudaStreamEndCapture(cs, &outer_body)) != cudaSuccess) return r;
+    return cudaGraphInstantiate(&ge, g, 0);
+  };
+  e = build();
+  if (e == cudaSuccess) e = cudaGraphLaunch(ge, st);
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return e;
 }
 
 // Adjoint over a trajectory for the wide neural ODE (Thomas solver); writes the
@@ -753,7 +977,7 @@ cudaError_t node_adjoint(const DevModel& m, const double* states, const double* 
     if ((e = node_eval(m, states, times, step_hi, -1, nb, P, H, Jb, true, st)) != cudaSuccess) return e;
     node_adj_rhs_kernel<<<blocks_for(P, 128), 128, 0, st>>>(states, times, Jb, dL, loss, lam, step_hi, c, nb, R);
     node_factor_kernel<<<blocks_for(P, 128), 128, 0, st>>>(Jb, times, step_hi, c, nb, 1, recs, sing_key, ord, nc,
-                                                             nullptr);
+                                                             nullptr, nullptr);
     const cudaError_t aattr = allow_smem((const void*)node_thomas_adj_kernel, kSubSmem);
     if (aattr != cudaSuccess) return aattr;
     node_thomas_adj_kernel<<<blocks_for(nb, kSubThreads), kSubThreads, kSubSmem, st>>>(R, recs, times, step_hi, c,
@@ -762,6 +986,18 @@ cudaError_t node_adjoint(const DevModel& m, const double* states, const double* 
     ++ord;
   }
   return cudaGetLastError();
+}
+
+cudaError_t preload_node_kernels() {
+  using namespace node;
+  for (const void* f : {(const void*)ctl_newton_start, (const void*)ctl_newton_iter, (const void*)ctl_newton_end,
+                        (const void*)ctl_chunk_end, (const void*)node_eval_kernel, (const void*)node_residual_kernel,
+                        (const void*)node_residual_pp_kernel, (const void*)node_factor_kernel,
+                        (const void*)node_thomas_fwd_kernel, (const void*)node_adj_rhs_kernel,
+                        (const void*)node_thomas_adj_kernel, (const void*)node_init_chunk_kernel,
+                        (const void*)node_group_flags_kernel, (const void*)node_vectors_dmma_kernel})
+    if (cudaError_t e = preload(f)) return e;
+  return cudaSuccess;
 }
 
 }  // namespace cko
