@@ -576,6 +576,68 @@ __device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* v
   for (int i = 0; i < N; ++i) v[i] = y[i];
 }
 
+// The consumer's lane split over a group of TPL threads: thread gt of the group
+// holds rows gt, gt + TPL, ... (R of them), so one lane's substitution chain
+// advances TPL rows per step instead of one.
+#ifndef CKO_COOP_CONSUMER
+#define CKO_COOP_CONSUMER 1  // knob: 0 = one thread per lane (lu_solve_rec)
+#endif
+template <int N, int TPL>
+struct Coop {
+  static constexpr int R = (N + TPL - 1) / TPL;
+};
+
+// v <- M^{-1} v (lu_solve_vec, linalg.cpp:46-60) on a TPL-thread group: the
+// permuted gather goes through the lane's shared scratch `vs`; every finished
+// entry is broadcast to the group by a shuffle. The forward sweep subtracts
+// in the reference's order (j ascending); the backward sweep finishes y_j and
+// then removes it from the rows above (the same rounding-level reordering as
+// lu_solve_rec).
+template <int N, int TPL>
+__device__ __forceinline__ void lu_solve_coop(const double* __restrict__ rec, double* vs,
+                                              double (&y)[Coop<N, TPL>::R], int gt, int gbase, bool writer) {
+  constexpr int R = Coop<N, TPL>::R;
+  const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
+  if (!perm[N]) {
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int i = gt + s * TPL;
+      if (writer && i < N) vs[i] = y[s];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int i = gt + s * TPL;
+      if (i < N) y[s] = vs[perm[i]];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < N - 1; ++j) {
+    const double yj = __shfl_sync(0xffffffffu, y[j / TPL], gbase + j % TPL);
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int i = gt + s * TPL;
+      if (s * TPL + TPL - 1 > j && i > j && i < N) y[s] -= rec[i * N + j] * yj;
+    }
+  }
+#pragma unroll
+  for (int j = N - 1; j >= 0; --j) {
+    if (gt == j % TPL) y[j / TPL] *= rec[Rec<N>::RD + j];
+    const double yj = __shfl_sync(0xffffffffu, y[j / TPL], gbase + j % TPL);
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int i = gt + s * TPL;
+      if (s * TPL < j && i < j) y[s] -= rec[i * N + j] * yj;
+    }
+  }
+}
+
+// Threads per lane for a tile of LTc lanes (the largest power of two that fits the warp).
+__device__ __forceinline__ int coop_tpl(int LTc) {
+  return LTc <= 1 ? 32 : LTc <= 2 ? 16 : LTc <= 4 ? 8 : LTc <= 8 ? 4 : LTc <= 16 ? 2 : 1;
+}
+
 template <int N>
 __device__ __forceinline__ void load_vec(const double* __restrict__ p, double (&v)[N]) {
 #pragma unroll
@@ -848,6 +910,47 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       if (tr) tr[3] = globaltimer_ns();
       bar_arrive(1 + q, nthr);
     }
+  } else if (warp == 0 && CKO_COOP_CONSUMER) {
+    // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, each lane on a group of threads
+    const int tpl = coop_tpl(LTc);
+    auto run = [&](auto tag) {
+      constexpr int TPL = decltype(tag)::value;
+      constexpr int R = Coop<N, TPL>::R;
+      const int lt = lane / TPL, gt = lane % TPL, gbase = lt * TPL;
+      const bool active = lt < LTc;
+      const int ltc = active ? lt : LTc - 1;  // idle groups shadow the last lane (no stores)
+      const int b = x.lb0 + t0 + ltc;
+      double* vs = vss + (size_t)ltc * N;
+      double xv[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) xv[q] = 0.0;
+      RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
+      for (int k = 0; k < x.c; ++k) {
+        ring.acquire(k);
+        const double* rec = recs + (size_t)ring.record(k, ltc) * Rec<N>::STRIDE;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (i < N) xv[q] = rec[Rec<N>::RHS + i] + xv[q];
+        }
+        lu_solve_coop<N, TPL>(rec, vs, xv, gt, gbase, active);
+        double* yy = a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (active && i < N) yy[i] = rec[Rec<N>::Y + i] - xv[q];
+        }
+        ring.release(k);
+      }
+    };
+    switch (tpl) {
+      case 32: run(std::integral_constant<int, 32>{}); break;
+      case 16: run(std::integral_constant<int, 16>{}); break;
+      case 8: run(std::integral_constant<int, 8>{}); break;
+      case 4: run(std::integral_constant<int, 4>{}); break;
+      case 2: run(std::integral_constant<int, 2>{}); break;
+      default: run(std::integral_constant<int, 1>{}); break;
+    }
   } else if (warp == 0) {
     // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, one thread per lane
     const int lt = lane;
@@ -1102,6 +1205,55 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
       bar_arrive(1 + q, nthr);
     }
+  } else if (warp == 0 && CKO_COOP_CONSUMER) {
+    const int tpl = coop_tpl(LTc);
+    auto run = [&](auto tag) {
+      constexpr int TPL = decltype(tag)::value;
+      constexpr int R = Coop<N, TPL>::R;
+      const int lt = lane / TPL, gt = lane % TPL, gbase = lt * TPL;
+      const bool active = lt < LTc;
+      const int ltc = active ? lt : LTc - 1;
+      const int b = lb0 + t0 + ltc;
+      double* vs = vss + (size_t)ltc * N;
+      const double* lc = lam + (size_t)ltc * N;
+      double d[R];  // delta_{r-1}, then delta_r
+#pragma unroll
+      for (int q = 0; q < R; ++q) d[q] = 0.0;
+      RingConsumer ring(sh.RS, Q, LTc, c, nthr);
+      for (int r = 0; r < c; ++r) {
+        ring.acquire(r);
+        const double* rec = recs + (size_t)ring.record(r, ltc) * Rec<N>::STRIDE;
+        const int m = step_hi - r;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (i < N) d[q] = rec[Rec<N>::RHS + i] + d[q];
+        }
+        const double dt = rec[Rec<N>::DT];
+        lu_solve_coop<N, TPL>(rec, vs, d, gt, gbase, active);
+        double* w = a.wq + (size_t)m * row + (size_t)b * N;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (active && i < N) w[i] = (lc[i] + d[q]) * dt;
+        }
+        ring.release(r);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < R; ++q) {  // the new carry's increment, for the caller (adjoint.cpp:121-126)
+        const int i = gt + q * TPL;
+        if (active && i < N) vs[i] = d[q];
+      }
+    };
+    switch (tpl) {
+      case 32: run(std::integral_constant<int, 32>{}); break;
+      case 16: run(std::integral_constant<int, 16>{}); break;
+      case 8: run(std::integral_constant<int, 8>{}); break;
+      case 4: run(std::integral_constant<int, 4>{}); break;
+      case 2: run(std::integral_constant<int, 2>{}); break;
+      default: run(std::integral_constant<int, 1>{}); break;
+    }
   } else if (warp == 0) {
     const int lt = lane;
     const bool active = lt < LTc;
@@ -1160,7 +1312,9 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
       double dcar[N];
       adj_epoch<MS>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
       __syncthreads();
-      if (consumer && lane < LTc) {  // new carry (adjoint.cpp:121-126)
+      if (CKO_COOP_CONSUMER) {  // new carry (adjoint.cpp:121-126): the increments the consumer left in vss
+        for (int i = threadIdx.x; i < LTc * N; i += blockDim.x) lam[i] += vss[i];
+      } else if (consumer && lane < LTc) {
 #pragma unroll
         for (int i = 0; i < N; ++i) lam[(size_t)lane * N + i] += dcar[i];
       }

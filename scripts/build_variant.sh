@@ -15,10 +15,11 @@ OBJS=""
 for f in "$OBJ"/*.o; do
   b=$(basename "$f" .o)
   case $b in
-    cko_inst_*) nvcc $FLAGS $DEFS -c "$SRC/$b.cu" -o "$OUT/$b.o"; OBJS="$OBJS $OUT/$b.o" ;;
+    cko_inst_*) nvcc $FLAGS $DEFS -c "$SRC/$b.cu" -o "$OUT/$b.o" & OBJS="$OBJS $OUT/$b.o" ;;
     *) OBJS="$OBJS $f" ;;
   esac
 done
-nvcc -gencode arch=compute_100a,code=sm_100a -shared $OBJS -o "$ROOT/variants/$NAME.so" -lcudart
+wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared $OBJS -o "$ROOT/variants/$NAME.so" -lcudart -lpthread
 rm -rf "$OUT"
 echo "variants/$NAME.so"
