@@ -580,7 +580,7 @@ __device__ inline void lu_solve_rec(const double* __restrict__ rec_in, double* v
 // holds rows gt, gt + TPL, ... (R of them), so one lane's substitution chain
 // advances TPL rows per step instead of one.
 #ifndef CKO_COOP_CONSUMER
-#define CKO_COOP_CONSUMER 1  // knob: 0 = one thread per lane (lu_solve_rec)
+#define CKO_COOP_CONSUMER 0  // knob: 1 = each lane on a thread group (measured: no gain, adjoint slower)
 #endif
 template <int N, int TPL>
 struct Coop {
