@@ -97,6 +97,10 @@ constexpr bool kFwdSharedJac = CKO_FWD_SHARED_JAC;
 constexpr bool kFwdSlotRows = CKO_FWD_SLOT_ROWS;
 constexpr bool kFwdPred = CKO_FWD_PRED;
 constexpr int kMaxWs = 3;     // producer warps per slot
+#ifndef CKO_INV_MAX_LANES
+#define CKO_INV_MAX_LANES 2  // knob: explicit-inverse records up to this many lanes per CTA (0: never)
+#endif
+constexpr int kInvMaxLanes = CKO_INV_MAX_LANES;
 
 // Shared-memory record of one factored point (doubles): the LU factors in
 // the reference's row order (row-major), 1/U_ii, rhs (residual / adjoint
@@ -114,6 +118,10 @@ struct Rec {
   static constexpr int PERM = DT + 1;                       // ints start here (as double offset)
   static constexpr int RAW = PERM + (N + 2) / 2;
   static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
+  // explicit-inverse records (small lane counts, see lu_inverse_group): M^{-1} row-major after the rest
+  static constexpr int INV = ((RAW + 1) / 2) * 2;
+  static constexpr int RAW_INV = INV + N * N;
+  static constexpr int STRIDE_INV = RAW_INV + ((2 - RAW_INV % 16) + 16) % 16;
 };
 
 // Models whose Jacobian is a per-CTA constant in shared memory (MdsS).
@@ -148,15 +156,17 @@ struct Shape {
   int RS;              // records per slot (= groups per set)
   int threads;
   int smem_bytes;
+  int inv;             // records carry M^{-1} and the consumer multiplies (few lanes per CTA)
+  int stride;          // record stride in doubles (Rec<N>::STRIDE or STRIDE_INV)
 };
 
 template <class MS>
-__host__ __device__ inline void smem_layout(int S, int Q, int Ws, int RS, int LT, int& o_cs, int& o_rec, int& o_pb, int& o_vs,
-                                            int& o_lam, int& total_doubles) {
+__host__ __device__ inline void smem_layout(int S, int Q, int Ws, int RS, int LT, int stride, int& o_cs, int& o_rec,
+                                            int& o_pb, int& o_vs, int& o_lam, int& total_doubles) {
   constexpr int N = MS::N;
   o_cs = 0;
   o_rec = ((MS::NCONST + 1) / 2) * 2;
-  o_pb = o_rec + Q * RS * Rec<N>::STRIDE;
+  o_pb = o_rec + Q * RS * stride;
   const int groups = S * RS;
   o_vs = o_pb + groups * kPb<N>;
   o_lam = o_vs + LT * N + (N & 1);
@@ -633,6 +643,60 @@ __device__ __forceinline__ void lu_solve_coop(const double* __restrict__ rec, do
   }
 }
 
+// M^{-1} from the factors in `rec` (P M = L U): lane gl of the block's group
+// solves M x = e_j for its columns j = gl, gl + G, ... (L y = P e_j, U x = y,
+// the reference's substitution order) and writes them to rec[INV]. The
+// consumer then applies M^{-1} as one matrix-vector product whose rows are
+// independent, instead of a 2N-long dependent substitution chain.
+template <int N>
+__device__ inline void lu_inverse_group(double* rec, int gl) {
+  constexpr int G = Geo<N>::G;
+  const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
+  const bool ident = perm[N] != 0;
+  double* inv = rec + Rec<N>::INV;
+  // the column lives in its final place in shared memory while it is solved (no register arrays: the
+  // producer's registers are spent on the group LU)
+  for (int j = gl; j < N; j += G) {
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      double t = (ident ? i == j : perm[i] == j) ? 1.0 : 0.0;
+#pragma unroll 4
+      for (int k = 0; k < i; ++k) t -= rec[i * N + k] * inv[k * N + j];
+      inv[i * N + j] = t;
+    }
+#pragma unroll 1
+    for (int i = N - 1; i >= 0; --i) {
+      double t = inv[i * N + j];
+#pragma unroll 4
+      for (int k = i + 1; k < N; ++k) t -= rec[i * N + k] * inv[k * N + j];
+      inv[i * N + j] = t * rec[Rec<N>::RD + i];
+    }
+  }
+}
+
+// x <- M^{-1} v with the lane's rows on a TPL-thread group: every v_j is
+// broadcast once, each thread forms its rows' dot products (j ascending).
+template <int N, int TPL>
+__device__ __forceinline__ void inv_apply_coop(const double* __restrict__ rec, double (&v)[Coop<N, TPL>::R], int gt,
+                                               int gbase) {
+  constexpr int R = Coop<N, TPL>::R;
+  const double* inv = rec + Rec<N>::INV;
+  double acc[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) acc[q] = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const double vj = __shfl_sync(0xffffffffu, v[j / TPL], gbase + j % TPL);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = gt + q * TPL;
+      if (i < N) acc[q] += inv[i * N + j] * vj;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < R; ++q) v[q] = acc[q];
+}
+
 // Threads per lane for a tile of LTc lanes (the largest power of two that fits the warp).
 __device__ __forceinline__ int coop_tpl(int LTc) {
   return LTc <= 1 ? 32 : LTc <= 2 ? 16 : LTc <= 4 ? 8 : LTc <= 8 ? 4 : LTc <= 16 ? 2 : 1;
@@ -834,7 +898,7 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
 }
 
 // One Newton iteration over the rows of one lane tile (integrate.cpp:208-231).
-template <class MS>
+template <class MS, bool INV>
 __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, const double* cs, double* recs,
                           double* pbs, double* vss, const double* hr, int t0, int LTc, unsigned* s_sing) {
   constexpr int N = MS::N;
@@ -863,7 +927,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
       const int item = active ? js * RS + gi : I - 1;
       const int k = item / LTc, lb = t0 + item % LTc, b = x.lb0 + lb;
-      double* rec = recs + (size_t)(q * RS + gi) * Rec<N>::STRIDE;
+      double* rec = recs + (size_t)(q * RS + gi) * sh.stride;
       unsigned long long* tr = (tr0 && js < x.c) ? tr0 + js * 8 : nullptr;  // slot js: tr[js * 8 + 0..3]
       if (tr) tr[0] = globaltimer_ns();
       if (js >= Q) bar_sync(1 + Q + q, nthr);
@@ -907,9 +971,50 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
         atomicMin(a.sing_key, (unsigned long long)k * nb + b);
         atomicOr(s_sing, 1u);
       }
+      if constexpr (INV) {
+        __syncwarp();
+        lu_inverse_group<N>(rec, gl);
+      }
       if (tr) tr[3] = globaltimer_ns();
       bar_arrive(1 + q, nthr);
     }
+  } else if (INV && warp == 0) {
+    // ---- consumer with explicit inverses: x_k = M_k^{-1}(r_k + x_{k-1}) as one product, each lane on a group
+    const int tpl = coop_tpl(LTc);
+    auto run = [&](auto tag) {
+      constexpr int TPL = decltype(tag)::value;
+      constexpr int R = Coop<N, TPL>::R;
+      const int lt = lane / TPL, gt = lane % TPL, gbase = lt * TPL;
+      const bool active = lt < LTc;
+      const int ltc = active ? lt : LTc - 1;
+      const int b = x.lb0 + t0 + ltc;
+      double xv[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) xv[q] = 0.0;
+      RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
+      for (int k = 0; k < x.c; ++k) {
+        ring.acquire(k);
+        const double* rec = recs + (size_t)ring.record(k, ltc) * sh.stride;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (i < N) xv[q] = rec[Rec<N>::RHS + i] + xv[q];
+        }
+        inv_apply_coop<N, TPL>(rec, xv, gt, gbase);
+        double* yy = a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = gt + q * TPL;
+          if (active && i < N) yy[i] = rec[Rec<N>::Y + i] - xv[q];
+        }
+        ring.release(k);
+      }
+    };
+    static_assert(kInvMaxLanes <= 2, "explicit-inverse consumers are instantiated for 1 or 2 lanes per tile");
+    if (tpl == 32)
+      run(std::integral_constant<int, 32>{});
+    else
+      run(std::integral_constant<int, 16>{});
   } else if (warp == 0 && CKO_COOP_CONSUMER) {
     // ---- consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, each lane on a group of threads
     const int tpl = coop_tpl(LTc);
@@ -927,7 +1032,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
       for (int k = 0; k < x.c; ++k) {
         ring.acquire(k);
-        const double* rec = recs + (size_t)ring.record(k, ltc) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(k, ltc) * sh.stride;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int i = gt + q * TPL;
@@ -967,7 +1072,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       ring.acquire(k);
       if (tr) tr[k * 8 + 5] = globaltimer_ns();
       if (active) {
-        const double* rec = recs + (size_t)ring.record(k, lt) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(k, lt) * sh.stride;
 #pragma unroll
         for (int i = 0; i < N; ++i) xv[i] = rec[Rec<N>::RHS + i] + xv[i];
         lu_solve_rec<N>(rec, vs, xv);
@@ -981,13 +1086,13 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
   }
 }
 
-template <class MS>
+template <class MS, bool INV>
 __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned s_bcast, s_flags, s_sing;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -999,7 +1104,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   x.row = (size_t)a.nb * N;
   double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
   // residual staging: the record ring (idle between epochs)
-  const int ring_doubles = sh.Q * sh.RS * Rec<N>::STRIDE;
+  const int ring_doubles = sh.Q * sh.RS * sh.stride;
   double* nrm = hr + (size_t)a.slab.Pmax * N;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
@@ -1047,7 +1152,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
       ++it;
       if (ktr && it < 4) ktr[2 + 3 * (it - 1)] = globaltimer_ns();
       for (int t0 = 0; t0 < x.L; t0 += sh.LT) {
-        fwd_epoch<MS>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
+        fwd_epoch<MS, INV>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
         __syncthreads();
       }
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
@@ -1083,7 +1188,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
 // dt J^T lambda_c, M_r = (I - J dt)^T, LU. Consumer: delta_r = M_r^{-1}(rhs_r +
 // delta_{r-1}), quadrature weight w_m = (lambda_c + delta_r) dt, and the new
 // carry lambda_c += delta_{c-1}.
-template <class MS>
+template <class MS, bool INV>
 __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs, double* recs, double* pbs,
                           double* vss, double* lam, int lb0, int t0, int LTc, int step_hi, int c, double Lval,
                           unsigned long long ord, double (&dcar)[MS::N]) {
@@ -1113,7 +1218,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       const int r = item / LTc, ltc = item % LTc;
       const int b = lb0 + t0 + ltc;
       const double* lm = lam + (size_t)ltc * N;
-      double* rec = recs + (size_t)(q * RS + gi) * Rec<N>::STRIDE;
+      double* rec = recs + (size_t)(q * RS + gi) * sh.stride;
       if (js >= Q) bar_sync(1 + Q + q, nthr);
       const int m = step_hi - r;
       const double t = a.times[(size_t)m * nb + b];
@@ -1203,10 +1308,15 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         fok = factor_block<N, true>(build, rows, gl, gr.base, pb, rec);
       if (!fok && active && gl == 0)
         atomicMin(a.sing_key, ord * (unsigned long long)a.nc * nb + (unsigned long long)r * nb + b);
+      if constexpr (INV) {
+        __syncwarp();
+        lu_inverse_group<N>(rec, gl);
+      }
       bar_arrive(1 + q, nthr);
     }
-  } else if (warp == 0 && CKO_COOP_CONSUMER) {
+  } else if ((INV || CKO_COOP_CONSUMER) && warp == 0) {
     const int tpl = coop_tpl(LTc);
+    constexpr bool use_inv = INV;
     auto run = [&](auto tag) {
       constexpr int TPL = decltype(tag)::value;
       constexpr int R = Coop<N, TPL>::R;
@@ -1222,7 +1332,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       RingConsumer ring(sh.RS, Q, LTc, c, nthr);
       for (int r = 0; r < c; ++r) {
         ring.acquire(r);
-        const double* rec = recs + (size_t)ring.record(r, ltc) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(r, ltc) * sh.stride;
         const int m = step_hi - r;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -1230,7 +1340,10 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
           if (i < N) d[q] = rec[Rec<N>::RHS + i] + d[q];
         }
         const double dt = rec[Rec<N>::DT];
-        lu_solve_coop<N, TPL>(rec, vs, d, gt, gbase, active);
+        if constexpr (use_inv)
+          inv_apply_coop<N, TPL>(rec, d, gt, gbase);
+        else
+          lu_solve_coop<N, TPL>(rec, vs, d, gt, gbase, active);
         double* w = a.wq + (size_t)m * row + (size_t)b * N;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -1246,13 +1359,20 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         if (active && i < N) vs[i] = d[q];
       }
     };
-    switch (tpl) {
-      case 32: run(std::integral_constant<int, 32>{}); break;
-      case 16: run(std::integral_constant<int, 16>{}); break;
-      case 8: run(std::integral_constant<int, 8>{}); break;
-      case 4: run(std::integral_constant<int, 4>{}); break;
-      case 2: run(std::integral_constant<int, 2>{}); break;
-      default: run(std::integral_constant<int, 1>{}); break;
+    if constexpr (INV) {  // 1 or 2 lanes per tile (kInvMaxLanes)
+      if (tpl == 32)
+        run(std::integral_constant<int, 32>{});
+      else
+        run(std::integral_constant<int, 16>{});
+    } else {
+      switch (tpl) {
+        case 32: run(std::integral_constant<int, 32>{}); break;
+        case 16: run(std::integral_constant<int, 16>{}); break;
+        case 8: run(std::integral_constant<int, 8>{}); break;
+        case 4: run(std::integral_constant<int, 4>{}); break;
+        case 2: run(std::integral_constant<int, 2>{}); break;
+        default: run(std::integral_constant<int, 1>{}); break;
+      }
     }
   } else if (warp == 0) {
     const int lt = lane;
@@ -1267,7 +1387,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     for (int r = 0; r < c; ++r) {
       ring.acquire(r);
       if (active) {
-        const double* rec = recs + (size_t)ring.record(r, lt) * Rec<N>::STRIDE;
+        const double* rec = recs + (size_t)ring.record(r, lt) * sh.stride;
         const int m = step_hi - r;
 #pragma unroll
         for (int i = 0; i < N; ++i) d[i] = rec[Rec<N>::RHS + i] + d[i];
@@ -1284,12 +1404,12 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   }
 }
 
-template <class MS>
+template <class MS, bool INV>
 __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -1310,9 +1430,9 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
     while (step_hi >= 1) {
       const int c = min(a.nc, step_hi);
       double dcar[N];
-      adj_epoch<MS>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
+      adj_epoch<MS, INV>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
       __syncthreads();
-      if (CKO_COOP_CONSUMER) {  // new carry (adjoint.cpp:121-126): the increments the consumer left in vss
+      if (INV || CKO_COOP_CONSUMER) {  // new carry (adjoint.cpp:121-126): the increments left in vss
         for (int i = threadIdx.x; i < LTc * N; i += blockDim.x) lam[i] += vss[i];
       } else if (consumer && lane < LTc) {
 #pragma unroll
@@ -1345,11 +1465,18 @@ inline Shape make_shape(int L) {
   // Two record slots per set when they fit: a set factors slot j + S while the
   // consumer still reads slot j, so the producers never wait on the solve.
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  for (sh.Q = 2 * sh.S;; sh.Q = sh.S) {
-    // a tile row must never need a slot more than Q - 1 slots past the oldest unreleased one
-    sh.LT = min(min(32, L), (sh.Q - 1) * sh.RS);  // no wider than the CTA's lanes (shared memory)
-    smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
-    if (sh.Q == sh.S || (sh.Q <= kMaxSlots && tot * 8 <= kSmemCap)) break;
+  // Few lanes per CTA (the strong-scaled shapes): the substitution chain, one 20x20 solve per row on a
+  // single thread, is the critical path while the producers idle, so the records carry M^{-1} and the
+  // consumer multiplies (lu_inverse_group); otherwise the plain LU records.
+  for (sh.inv = L <= kInvMaxLanes ? 1 : 0; sh.inv >= 0; --sh.inv) {
+    sh.stride = sh.inv ? Rec<N>::STRIDE_INV : Rec<N>::STRIDE;
+    for (sh.Q = 2 * sh.S;; sh.Q = sh.S) {
+      // a tile row must never need a slot more than Q - 1 slots past the oldest unreleased one
+      sh.LT = min(min(32, L), (sh.Q - 1) * sh.RS);  // no wider than the CTA's lanes (shared memory)
+      smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+      if (sh.Q == sh.S || (sh.Q <= kMaxSlots && tot * 8 <= kSmemCap)) break;
+    }
+    if (tot * 8 <= kSmemCap || sh.inv == 0) break;
   }
   sh.smem_bytes = tot * 8;
   return sh;
@@ -1357,23 +1484,34 @@ inline Shape make_shape(int L) {
 
 template <class MS>
 cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
-  if (!a) return preload((const void*)fwd2_kernel<MS>);  // probe: also loads the kernel (lazy module loading)
+  if (!a) {  // probe: also loads the kernels (lazy module loading)
+    const cudaError_t e = preload((const void*)fwd2_kernel<MS, false>);
+    return e != cudaSuccess ? e : preload((const void*)fwd2_kernel<MS, true>);
+  }
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   Shape sh = make_shape<MS>(Lmax);
-  CKO_ALLOW_FULL_SMEM(fwd2_kernel<MS>);
+  const void* k = sh.inv ? (const void*)fwd2_kernel<MS, true> : (const void*)fwd2_kernel<MS, false>;
+  CKO_ALLOW_FULL_SMEM(k);
   FwdLaunch copy = *a;
   void* args[] = {&copy, &sh};
-  return launch_persistent((const void*)fwd2_kernel<MS>, dim3(a->grid), dim3(sh.threads), args,
-                                     sh.smem_bytes, st);
+  return launch_persistent(k, dim3(a->grid), dim3(sh.threads), args, sh.smem_bytes, st);
 }
 
 template <class MS>
 cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
-  if (!a) return preload((const void*)adj2_kernel<MS>);
+  if (!a) {
+    const cudaError_t e = preload((const void*)adj2_kernel<MS, false>);
+    return e != cudaSuccess ? e : preload((const void*)adj2_kernel<MS, true>);
+  }
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   Shape sh = make_shape<MS>(Lmax);
-  CKO_ALLOW_FULL_SMEM(adj2_kernel<MS>);
-  adj2_kernel<MS><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
+  if (sh.inv) {
+    CKO_ALLOW_FULL_SMEM((adj2_kernel<MS, true>));
+    adj2_kernel<MS, true><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
+  } else {
+    CKO_ALLOW_FULL_SMEM((adj2_kernel<MS, false>));
+    adj2_kernel<MS, false><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
+  }
   return cudaGetLastError();
 }
 
