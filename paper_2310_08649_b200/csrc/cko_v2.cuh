@@ -146,7 +146,7 @@ struct HasSlotRows<MS, std::void_t<decltype(MS::kSlotRows)>> {
 
 // Per-group pivot-row buffer: two rows of N + 2 doubles (16-byte aligned halves).
 template <int N>
-constexpr int kPbRow = N + 2;
+constexpr int kPbRow = ((N + 3) / 2) * 2;  // even: both halves stay 16-byte aligned for the pair stores
 template <int N>
 constexpr int kPb = 2 * kPbRow<N>;
 
@@ -648,30 +648,70 @@ __device__ __forceinline__ void lu_solve_coop(const double* __restrict__ rec, do
 // the reference's substitution order) and writes them to rec[INV]. The
 // consumer then applies M^{-1} as one matrix-vector product whose rows are
 // independent, instead of a 2N-long dependent substitution chain.
+#ifndef CKO_INV_FENCE
+#define CKO_INV_FENCE 0  // knob: compiler fence between the factor rows of the inverse (measured: slower)
+#endif
 template <int N>
 __device__ inline void lu_inverse_group(double* rec, int gl) {
   constexpr int G = Geo<N>::G;
+  constexpr int NC = (N + G - 1) / G;  // columns per lane
   const int* perm = reinterpret_cast<const int*>(rec + Rec<N>::PERM);
   const bool ident = perm[N] != 0;
   double* inv = rec + Rec<N>::INV;
-  // the column lives in its final place in shared memory while it is solved (no register arrays: the
-  // producer's registers are spent on the group LU)
-  for (int j = gl; j < N; j += G) {
-#pragma unroll 1
-    for (int i = 0; i < N; ++i) {
-      double t = (ident ? i == j : perm[i] == j) ? 1.0 : 0.0;
-#pragma unroll 4
-      for (int k = 0; k < i; ++k) t -= rec[i * N + k] * inv[k * N + j];
-      inv[i * N + j] = t;
-    }
-#pragma unroll 1
-    for (int i = N - 1; i >= 0; --i) {
-      double t = inv[i * N + j];
-#pragma unroll 4
-      for (int k = i + 1; k < N; ++k) t -= rec[i * N + k] * inv[k * N + j];
-      inv[i * N + j] = t * rec[Rec<N>::RD + i];
+  // the lane's columns side by side in registers (independent chains); each factor row is loaded once per
+  // step behind a compiler fence, so the loads are not all hoisted (the producer's registers are tight)
+  double y[NC][N];
+  int col[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    col[c] = gl + c * G;
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[c][i] = (col[c] < N && (ident ? i == col[c] : perm[i] == col[c])) ? 1.0 : 0.0;
+  }
+#pragma unroll
+  for (int i = 1; i < N; ++i) {  // L y = P e_j (unit lower)
+    if (CKO_INV_FENCE) asm volatile("" ::: "memory");
+    double li[N];
+#pragma unroll
+    for (int k = 0; k < i; ++k) li[k] = rec[i * N + k];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double t0 = y[c][i], t1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        if (k & 1)
+          t1 -= li[k] * y[c][k];
+        else
+          t0 -= li[k] * y[c][k];
+      }
+      y[c][i] = t0 + t1;
     }
   }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {  // U x = y
+    if (CKO_INV_FENCE) asm volatile("" ::: "memory");
+    double ui[N];
+#pragma unroll
+    for (int k = i + 1; k < N; ++k) ui[k] = rec[i * N + k];
+    const double rd = rec[Rec<N>::RD + i];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double t0 = y[c][i], t1 = 0.0;
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) {
+        if (k & 1)
+          t1 -= ui[k] * y[c][k];
+        else
+          t0 -= ui[k] * y[c][k];
+      }
+      y[c][i] = (t0 + t1) * rd;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    if (col[c] < N)
+#pragma unroll
+      for (int i = 0; i < N; ++i) inv[i * N + col[c]] = y[c][i];
 }
 
 // x <- M^{-1} v with the lane's rows on a TPL-thread group: every v_j is
@@ -902,6 +942,7 @@ template <class MS, bool INV>
 __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, const double* cs, double* recs,
                           double* pbs, double* vss, const double* hr, int t0, int LTc, unsigned* s_sing) {
   constexpr int N = MS::N;
+  constexpr int kStride = INV ? Rec<N>::STRIDE_INV : Rec<N>::STRIDE;
   using Gm = Geo<N>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = sh.S, Q = sh.Q, Ws = sh.Ws;
@@ -927,7 +968,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       const bool active = js * RS + gi < I;  // inactive groups factor a duplicate item, no side effects
       const int item = active ? js * RS + gi : I - 1;
       const int k = item / LTc, lb = t0 + item % LTc, b = x.lb0 + lb;
-      double* rec = recs + (size_t)(q * RS + gi) * sh.stride;
+      double* rec = recs + (size_t)(q * RS + gi) * kStride;
       unsigned long long* tr = (tr0 && js < x.c) ? tr0 + js * 8 : nullptr;  // slot js: tr[js * 8 + 0..3]
       if (tr) tr[0] = globaltimer_ns();
       if (js >= Q) bar_sync(1 + Q + q, nthr);
@@ -991,10 +1032,14 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       double xv[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) xv[q] = 0.0;
+      unsigned long long* tr =
+          (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
       RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
       for (int k = 0; k < x.c; ++k) {
+        if (tr) tr[k * 8 + 4] = globaltimer_ns();
         ring.acquire(k);
-        const double* rec = recs + (size_t)ring.record(k, ltc) * sh.stride;
+        if (tr) tr[k * 8 + 5] = globaltimer_ns();
+        const double* rec = recs + (size_t)ring.record(k, ltc) * kStride;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int i = gt + q * TPL;
@@ -1007,6 +1052,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
           const int i = gt + q * TPL;
           if (active && i < N) yy[i] = rec[Rec<N>::Y + i] - xv[q];
         }
+        if (tr) tr[k * 8 + 6] = globaltimer_ns();
         ring.release(k);
       }
     };
@@ -1032,7 +1078,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       RingConsumer ring(sh.RS, Q, LTc, x.c, nthr);
       for (int k = 0; k < x.c; ++k) {
         ring.acquire(k);
-        const double* rec = recs + (size_t)ring.record(k, ltc) * sh.stride;
+        const double* rec = recs + (size_t)ring.record(k, ltc) * kStride;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int i = gt + q * TPL;
@@ -1072,7 +1118,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       ring.acquire(k);
       if (tr) tr[k * 8 + 5] = globaltimer_ns();
       if (active) {
-        const double* rec = recs + (size_t)ring.record(k, lt) * sh.stride;
+        const double* rec = recs + (size_t)ring.record(k, lt) * kStride;
 #pragma unroll
         for (int i = 0; i < N; ++i) xv[i] = rec[Rec<N>::RHS + i] + xv[i];
         lu_solve_rec<N>(rec, vs, xv);
@@ -1089,6 +1135,7 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
 template <class MS, bool INV>
 __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
   constexpr int N = MS::N;
+  constexpr int kStride = INV ? Rec<N>::STRIDE_INV : Rec<N>::STRIDE;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned s_bcast, s_flags, s_sing;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
@@ -1104,7 +1151,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   x.row = (size_t)a.nb * N;
   double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
   // residual staging: the record ring (idle between epochs)
-  const int ring_doubles = sh.Q * sh.RS * sh.stride;
+  const int ring_doubles = sh.Q * sh.RS * kStride;
   double* nrm = hr + (size_t)a.slab.Pmax * N;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
@@ -1193,6 +1240,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
                           double* vss, double* lam, int lb0, int t0, int LTc, int step_hi, int c, double Lval,
                           unsigned long long ord, double (&dcar)[MS::N]) {
   constexpr int N = MS::N;
+  constexpr int kStride = INV ? Rec<N>::STRIDE_INV : Rec<N>::STRIDE;
   using Gm = Geo<N>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = sh.S, Q = sh.Q, Ws = sh.Ws;
@@ -1218,7 +1266,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       const int r = item / LTc, ltc = item % LTc;
       const int b = lb0 + t0 + ltc;
       const double* lm = lam + (size_t)ltc * N;
-      double* rec = recs + (size_t)(q * RS + gi) * sh.stride;
+      double* rec = recs + (size_t)(q * RS + gi) * kStride;
       if (js >= Q) bar_sync(1 + Q + q, nthr);
       const int m = step_hi - r;
       const double t = a.times[(size_t)m * nb + b];
@@ -1332,7 +1380,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       RingConsumer ring(sh.RS, Q, LTc, c, nthr);
       for (int r = 0; r < c; ++r) {
         ring.acquire(r);
-        const double* rec = recs + (size_t)ring.record(r, ltc) * sh.stride;
+        const double* rec = recs + (size_t)ring.record(r, ltc) * kStride;
         const int m = step_hi - r;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
@@ -1387,7 +1435,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
     for (int r = 0; r < c; ++r) {
       ring.acquire(r);
       if (active) {
-        const double* rec = recs + (size_t)ring.record(r, lt) * sh.stride;
+        const double* rec = recs + (size_t)ring.record(r, lt) * kStride;
         const int m = step_hi - r;
 #pragma unroll
         for (int i = 0; i < N; ++i) d[i] = rec[Rec<N>::RHS + i] + d[i];
