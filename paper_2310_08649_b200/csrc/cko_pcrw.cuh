@@ -38,6 +38,10 @@ struct WRec {
   static constexpr int STRIDE = XT + N + (N & 1);
 };
 
+#ifndef CKO_PCRW_LANES
+#define CKO_PCRW_LANES 1  // knob: lanes per tile (the tile's records should stay in L2)
+#endif
+constexpr int kPcrwLanes = CKO_PCRW_LANES;
 constexpr int kPcrwWarps = 12;  // 168 registers per thread (the producer group LU and the sweep rows)
 
 // Per-warp staging slot of the sweep: partner LU, 1/U_ii, perm, B_q, x_q.
@@ -289,14 +293,17 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
         return;
       }
       ++it;
+      // lanes in tiles of kPcrwLanes: a tile's c records stay L2-resident through the sweeps
+      for (int l0 = 0; l0 < x.L; l0 += kPcrwLanes) {
+      const int Lt = min(kPcrwLanes, x.L - l0);
       // assemble M = I - J dt and factor (assemble_factor, integrate.cpp:118-135), x = r: three points per warp
       {
         const GroupLane<N> gr(lane);
-        const int P = c * x.L;
+        const int P = c * Lt;
         for (int p0 = warp * Gm::GPW; p0 < P; p0 += kPcrwWarps * Gm::GPW) {
           const bool active = p0 + gr.g < P;
           const int p = active ? p0 + gr.g : P - 1;  // inactive groups factor a duplicate, no side effects
-          const int k = p / x.L, lb = p % x.L, b = x.lb0 + lb;
+          const int k = p / Lt, lb = l0 + p % Lt, b = x.lb0 + lb;
           // inactive groups factor a duplicate point into the warp's idle sweep slot (never the live record)
           double* rec = active ? ws + (size_t)p * WRec<N>::STRIDE : slots + (size_t)warp * WSlot<N>::STRIDE;
           double* pb = pbs + (size_t)(warp * Gm::GPW + gr.g) * kPb<N>;
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
           };
           const bool ok = factor_block<N, false>(build, build, gr.gl, gr.base, pb, rec);
           if (active) {
-            const double* r = hr + (size_t)p * N;
+            const double* r = hr + (size_t)(k * x.L + lb) * N;
 #pragma unroll
             for (int q = 0; q < Gm::R; ++q) {
               const int i = gr.gl + q * Gm::G;
@@ -338,15 +345,16 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
         }
       }
       __syncthreads();
-      pcrw_solve_cta<N>(ws, c, x.L, a.solver == 1 ? -1 : a.n_switch, slots);
-      for (int p = tid; p < c * x.L; p += T) {  // yy -= x
-        const int k = p / x.L, b = x.lb0 + p % x.L;
+      pcrw_solve_cta<N>(ws, c, Lt, a.solver == 1 ? -1 : a.n_switch, slots);
+      for (int p = tid; p < c * Lt; p += T) {  // yy -= x
+        const int k = p / Lt, b = x.lb0 + l0 + p % Lt;
         double* yy = a.states + (size_t)(step + 1 + k) * x.row + (size_t)b * N;
         const double* xv = ws + (size_t)p * WRec<N>::STRIDE + Rec<N>::RHS;
 #pragma unroll
         for (int i = 0; i < N; ++i) yy[i] -= xv[i];
       }
       __syncthreads();
+      }  // lane tiles
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
       f = residual2<MS>(a, x, cs, hr, nrm, slots, stage_cap, false, &s_flags) | fl;
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
@@ -393,14 +401,16 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) adj_pcrw_kernel(AdjLaunch 
   unsigned long long ord = 0;
   while (step_hi >= 1) {
     const int c = min(a.nc, step_hi);
+    for (int l0 = 0; l0 < L; l0 += kPcrwLanes) {  // lanes in tiles: the tile's records stay L2-resident
+    const int Lt = min(kPcrwLanes, L - l0);
     // gather + J + rhs_r = dL + dt J^T lambda + transposed LU (adjoint.cpp:53-81), three points per warp
     {
       const GroupLane<N> gr(lane);
-      const int P = c * L;
+      const int P = c * Lt;
       for (int p0 = warp * Gm::GPW; p0 < P; p0 += kPcrwWarps * Gm::GPW) {
         const bool active = p0 + gr.g < P;
         const int p = active ? p0 + gr.g : P - 1;
-        const int r = p / L, lb = p % L, b = lb0 + lb, m = step_hi - r;
+        const int r = p / Lt, lb = l0 + p % Lt, b = lb0 + lb, m = step_hi - r;
         double* rec = active ? ws + (size_t)p * WRec<N>::STRIDE : slots + (size_t)warp * WSlot<N>::STRIDE;
         double* pb = pbs + (size_t)(warp * Gm::GPW + gr.g) * kPb<N>;
         const double t = a.times[(size_t)m * nb + b];
@@ -465,10 +475,10 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) adj_pcrw_kernel(AdjLaunch 
       }
     }
     __syncthreads();
-    pcrw_solve_cta<N>(ws, c, L, a.solver == 1 ? -1 : a.n_switch, slots);
+    pcrw_solve_cta<N>(ws, c, Lt, a.solver == 1 ? -1 : a.n_switch, slots);
     // quadrature weights w_r = (carry + delta_r) dt_r (adjoint.cpp:103-113)
-    for (int p = tid; p < c * L; p += T) {
-      const int r = p / L, lb = p % L, b = lb0 + lb, m = step_hi - r;
+    for (int p = tid; p < c * Lt; p += T) {
+      const int r = p / Lt, lb = l0 + p % Lt, b = lb0 + lb, m = step_hi - r;
       const double dt = a.times[(size_t)m * nb + b] - a.times[(size_t)(m - 1) * nb + b];
       const double* d = ws + (size_t)p * WRec<N>::STRIDE + Rec<N>::RHS;
       const double* lc = lam + (size_t)lb * N;
@@ -477,9 +487,10 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) adj_pcrw_kernel(AdjLaunch 
       for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
     }
     __syncthreads();
-    for (int idx = tid; idx < L * N; idx += T)  // new carry (adjoint.cpp:121-126)
-      lam[idx] += ws[(size_t)((c - 1) * L + idx / N) * WRec<N>::STRIDE + Rec<N>::RHS + idx % N];
+    for (int idx = tid; idx < Lt * N; idx += T)  // new carry (adjoint.cpp:121-126)
+      lam[(size_t)l0 * N + idx] += ws[(size_t)((c - 1) * Lt + idx / N) * WRec<N>::STRIDE + Rec<N>::RHS + idx % N];
     __syncthreads();
+    }  // lane tiles
     step_hi -= c;
     ++ord;
   }
