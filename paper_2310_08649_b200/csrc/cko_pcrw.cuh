@@ -38,10 +38,11 @@ struct WRec {
   static constexpr int STRIDE = XT + N + (N & 1);
 };
 
-#ifndef CKO_PCRW_LANES
-#define CKO_PCRW_LANES 1  // knob: lanes per tile (the tile's records should stay in L2)
+#ifndef CKO_PCRW_ROWS
+#define CKO_PCRW_ROWS 64  // knob: records per lane tile (c x lanes; the tile stays in L2, the warps stay busy)
 #endif
-constexpr int kPcrwLanes = CKO_PCRW_LANES;
+constexpr int kPcrwRows = CKO_PCRW_ROWS;
+__device__ __forceinline__ int pcrw_tile_lanes(int c) { return c >= kPcrwRows ? 1 : kPcrwRows / c; }
 constexpr int kPcrwWarps = 12;  // 168 registers per thread (the producer group LU and the sweep rows)
 
 // Per-warp staging slot of the sweep: partner LU, 1/U_ii, perm, B_q, x_q.
@@ -293,9 +294,10 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
         return;
       }
       ++it;
-      // lanes in tiles of kPcrwLanes: a tile's c records stay L2-resident through the sweeps
-      for (int l0 = 0; l0 < x.L; l0 += kPcrwLanes) {
-      const int Lt = min(kPcrwLanes, x.L - l0);
+      // lanes in tiles of ~kPcrwRows records: a tile stays L2-resident through the sweeps
+      const int LTW = pcrw_tile_lanes(c);
+      for (int l0 = 0; l0 < x.L; l0 += LTW) {
+      const int Lt = min(LTW, x.L - l0);
       // assemble M = I - J dt and factor (assemble_factor, integrate.cpp:118-135), x = r: three points per warp
       {
         const GroupLane<N> gr(lane);
@@ -401,8 +403,9 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) adj_pcrw_kernel(AdjLaunch 
   unsigned long long ord = 0;
   while (step_hi >= 1) {
     const int c = min(a.nc, step_hi);
-    for (int l0 = 0; l0 < L; l0 += kPcrwLanes) {  // lanes in tiles: the tile's records stay L2-resident
-    const int Lt = min(kPcrwLanes, L - l0);
+    const int LTW = pcrw_tile_lanes(c);
+    for (int l0 = 0; l0 < L; l0 += LTW) {  // lanes in tiles: the tile's records stay L2-resident
+    const int Lt = min(LTW, L - l0);
     // gather + J + rhs_r = dL + dt J^T lambda + transposed LU (adjoint.cpp:53-81), three points per warp
     {
       const GroupLane<N> gr(lane);
