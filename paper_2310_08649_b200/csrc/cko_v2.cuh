@@ -88,6 +88,9 @@ constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruct
 #ifndef CKO_FWD_SLOT_ROWS
 #define CKO_FWD_SLOT_ROWS 0  // forward builds MDS rows by kind (position / velocity slot)
 #endif
+#ifndef CKO_LU_SKIP
+#define CKO_LU_SKIP 1  // knob: skip a slot's trailing update when every multiplier in it is zero
+#endif
 #ifndef CKO_FWD_PRED
 #define CKO_FWD_PRED 0  // predicated (not branched) trailing update in the forward LU
 #endif
@@ -434,14 +437,30 @@ __device__ inline int lu_group(double (&a)[Geo<N>::R][N], int gl, int base, doub
     // slot s holds rows s G .. s G + G - 1: nothing below the pivot once c >= s G + G - 1.
     // kPred: predicated, not branched — rows on or above the pivot run the update with l = 0,
     // which leaves them unchanged (up to the sign of a zero entry). Measured per kernel.
+    // The reference skips a row whose multiplier is exactly zero (lu_factor_block's `if (l != 0.0)`,
+    // linalg.cpp:36-40): x - 0 y is x, so skipping is exact. Here the whole slot's update is skipped when no
+    // lane of the warp has a nonzero multiplier in it (the warp's blocks share a sparsity pattern, e.g. the
+    // MDS chain's I - dt J), which removes most of the chain matrices' trailing updates.
     auto update = [&](int s) {
       if constexpr (kPred) {
         if (s * G + G - 1 > c) {
           const bool below = gl + s * G > c && gl + s * G < N;
           const double l = below ? a[s][c] * inv : 0.0;
           if (below) a[s][c] = l;
+          if (!CKO_LU_SKIP || __any_sync(0xffffffffu, l != 0.0)) {
 #pragma unroll
-          for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+            for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+          }
+        }
+      } else if (CKO_LU_SKIP) {
+        if (s * G + G - 1 > c) {
+          const bool below = gl + s * G > c && gl + s * G < N;
+          const double l = below ? a[s][c] * inv : 0.0;
+          if (below) a[s][c] = l;
+          if (__any_sync(0xffffffffu, l != 0.0) && below) {
+#pragma unroll
+            for (int j = c + 1; j < N; ++j) a[s][j] -= l * buf[j];
+          }
         }
       } else if (s * G + G - 1 > c && gl + s * G > c && gl + s * G < N) {
         const double l = a[s][c] * inv;
