@@ -89,7 +89,7 @@ constexpr bool kFwdRounds = true;   // producer sets advance in rounds (instruct
 #define CKO_FWD_SLOT_ROWS 0  // forward builds MDS rows by kind (position / velocity slot)
 #endif
 #ifndef CKO_LU_SKIP
-#define CKO_LU_SKIP 1  // knob: skip a slot's trailing update when every multiplier in it is zero
+#define CKO_LU_SKIP 0  // knob: skip a slot's trailing update when every multiplier in it is zero (measured: slower)
 #endif
 #ifndef CKO_FWD_PRED
 #define CKO_FWD_PRED 0  // predicated (not branched) trailing update in the forward LU
