@@ -390,18 +390,13 @@ def c2_solver_family(args, local, nt_s=None, reps=1):
         sv = api.SolverChoice(kind, 1).c()
         tot = 0.0
         for it in range(reps + 1):
-            raise_for(L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()),
-                                              nb, nt_s, nc, C.byref(st), C.byref(sv),
-                                              C.c_void_p(d_states.data_ptr()), C.byref(wf), C.byref(e)), e)
-            L.cko_ctx_last_kernel_ms(ctx.h, kms)
-            f_ms = kms[0]
-            raise_for(L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()),
-                                              C.c_void_p(d_times.data_ptr()), nb, nt_s, nc, C.byref(sv),
-                                              abi.CKO_LOSS_FROBENIUS, None, C.byref(loss), abi.dptr(grad),
-                                              C.byref(wb), C.byref(e)), e)
+            raise_for(L.cko_gradient_adjoint_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()),
+                                                    C.c_void_p(d_times.data_ptr()), nb, nt_s, nc, C.byref(st),
+                                                    C.byref(sv), C.c_void_p(d_states.data_ptr()), C.byref(loss),
+                                                    abi.dptr(grad), C.byref(wf), C.byref(wb), C.byref(e)), e)
             L.cko_ctx_last_kernel_ms(ctx.h, kms)
             if it:  # the first pass warms up
-                tot += f_ms + kms[1] + kms[2] + kms[3]
+                tot += kms[0] + kms[1] + kms[2] + kms[3]
         ms = tot / reps
         out[name] = {"n_chunk": nc, "series_steps_per_s": nb * nt_s / (ms * 1e-3), "kernel_ms": ms,
                      "kernel_generation": ctx.kernel_generation_used()}
@@ -437,12 +432,10 @@ def north_star_strong(args, ctx, world, rank, stream, hbm_peak, reps=3, warmup=2
     wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
 
     def step():
-        raise_for(L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()),
-                                          nb, nt, sa.n_chunk, C.byref(st), C.byref(sv),
-                                          C.c_void_p(d_states.data_ptr()), C.byref(wf), C.byref(e)), e)
-        raise_for(L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()), C.c_void_p(d_times.data_ptr()),
-                                          nb, nt, sa.n_chunk, C.byref(sv), abi.CKO_LOSS_FROBENIUS, None,
-                                          C.byref(loss), abi.dptr(grad), C.byref(wb), C.byref(e)), e)
+        raise_for(L.cko_gradient_adjoint_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()),
+                                                C.c_void_p(d_times.data_ptr()), nb, nt, sa.n_chunk, C.byref(st),
+                                                C.byref(sv), C.c_void_p(d_states.data_ptr()), C.byref(loss),
+                                                abi.dptr(grad), C.byref(wf), C.byref(wb), C.byref(e)), e)
     for _ in range(warmup):
         step()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -539,24 +532,19 @@ def main():
     kms = (C.c_double * 4)()
 
     def step(record=None):
-        rc = L.cko_be_forward_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()), nb, nt,
-                                     args.n_chunk, C.byref(st), C.byref(sv), C.c_void_p(d_states.data_ptr()),
-                                     C.byref(wf), C.byref(e))
+        # one training step through the device-buffer gradient_adjoint: forward, loss, adjoint, parameter VJP
+        rc = L.cko_gradient_adjoint_device(ctx.h, dm, C.c_void_p(d_y0.data_ptr()), C.c_void_p(d_times.data_ptr()),
+                                           nb, nt, args.n_chunk, C.byref(st), C.byref(sv),
+                                           C.c_void_p(d_states.data_ptr()), C.byref(loss), abi.dptr(grad),
+                                           C.byref(wf), C.byref(wb), C.byref(e))
         raise_for(rc, e)
         if record is not None:
             L.cko_ctx_last_kernel_ms(ctx.h, kms)
             record["fwd"] += kms[0]
-            launches = L.cko_ctx_last_launches(ctx.h)
-        rc = L.cko_be_adjoint_device(ctx.h, dm, C.c_void_p(d_states.data_ptr()), C.c_void_p(d_times.data_ptr()),
-                                     nb, nt, args.n_chunk, C.byref(sv), abi.CKO_LOSS_FROBENIUS, None, C.byref(loss),
-                                     abi.dptr(grad), C.byref(wb), C.byref(e))
-        raise_for(rc, e)
-        if record is not None:
-            L.cko_ctx_last_kernel_ms(ctx.h, kms)
             record["adj"] += kms[1]
             record["vjp"] += kms[2]
             record["loss"] += kms[3]
-            record["launches"] += launches + L.cko_ctx_last_launches(ctx.h)
+            record["launches"] += L.cko_ctx_last_launches(ctx.h)
 
     for _ in range(args.warmup):
         step()

@@ -224,6 +224,17 @@ cko_status cko_gradient_adjoint(cko_ctx* ctx, const cko_model* model, const doub
                                 double* loss_out, double* grad_out, cko_work* fwd, cko_work* bwd,
                                 cko_error* err);
 
+/* Same over device buffers: d_y0 (nb, n) and d_times (nt+1, nb) in, the trajectory
+ * into d_states (nt+1, nb*n; d_states may alias d_y0 as its row 0); loss_out and
+ * grad_out (np) are host. One call is one training step: the Frobenius loss rides
+ * on the forward's residual passes instead of a separate pass over the trajectory. */
+cko_status cko_gradient_adjoint_device(cko_ctx* ctx, const cko_model* model, const double* d_y0,
+                                       const double* d_times, int nb, int nt, int n_chunk,
+                                       const cko_newton_settings* settings,
+                                       const cko_solver_choice* solver, double* d_states,
+                                       double* loss_out, double* grad_out, cko_work* fwd,
+                                       cko_work* bwd, cko_error* err);
+
 cko_status cko_traj_states(const cko_traj* traj, const double** d_states, int* nb, int* nt,
                            int* n);
 cko_status cko_traj_destroy(cko_traj* traj);

@@ -52,6 +52,8 @@ def lib() -> C.CDLL:
                                 C.c_int),
         "cko_be_adjoint_device": ([vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, P(S), C.c_int, vp, dp, dp, P(W), P(E)],
                                   C.c_int),
+        "cko_gradient_adjoint_device": ([vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, P(N), P(S), vp, dp, dp, P(W), P(W),
+                                         P(E)], C.c_int),
         "cko_gradient_adjoint": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, P(N), P(S), dp, dp, dp, P(W), P(W), P(E)],
                                  C.c_int),
         "cko_traj_states": ([vp, P(vp), P(C.c_int), P(C.c_int), P(C.c_int)], C.c_int),
@@ -77,7 +79,10 @@ def lib() -> C.CDLL:
         "cko_fe_adjoint_host": ([vp, vp, dp, dp, C.c_int, C.c_int, C.c_int, C.c_int, dp, dp, dp, P(W), P(E)],
                                 C.c_int),
     }
+    ab_build = bool(os.environ.get("CKO_LIB_PATH"))  # an A/B build may predate newer entry points
     for name, (args, res) in sig.items():
+        if ab_build and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -92,7 +97,7 @@ EXPORTS = [
     "cko_abi_version", "cko_model_state_size", "cko_model_param_count", "cko_ctx_create", "cko_ctx_destroy",
     "cko_ctx_set_stream", "cko_comm_buffer_bytes", "cko_ctx_set_group", "cko_model_create", "cko_model_destroy",
     "cko_be_forward", "cko_be_forward_device", "cko_be_adjoint", "cko_be_adjoint_host", "cko_be_adjoint_device",
-    "cko_gradient_adjoint", "cko_traj_states", "cko_traj_destroy", "cko_block_bidiag_solve",
+    "cko_gradient_adjoint", "cko_gradient_adjoint_device", "cko_traj_states", "cko_traj_destroy", "cko_block_bidiag_solve",
     "cko_newton_solve_chunk", "cko_ctx_enable_timing", "cko_ctx_last_kernel_ms", "cko_ctx_last_launches",
     "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open", "cko_ctx_set_kernel_generation",
     "cko_ctx_kernel_generation_used", "cko_chunk_residual", "cko_chunk_jacobian", "cko_adjoint_chunk_solve",

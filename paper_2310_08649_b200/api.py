@@ -391,6 +391,37 @@ def gradient_adjoint(model: Model, y0, grid: TimeGrid, n_chunk: int, loss: LossS
     return GradientResult(L.value, grad, tr, WorkCounters.from_c(wb))
 
 
+def gradient_adjoint_device(model: Model, d_y0, d_times, n_chunk: int, solver: SolverChoice | None = None,
+                            settings: NewtonSettings | None = None, ctx: Context | None = None, d_states=None):
+    """gradient_adjoint (adjoint.cpp:299-313, Frobenius loss) over CUDA tensors: d_y0 (nb, n) and d_times
+    (nt+1, nb) float64 on the context's device; the trajectory goes to d_states ((nt+1, nb*n), allocated when
+    None). One C call: the loss rides on the forward's residual passes. Returns (loss, gradient, d_states,
+    forward WorkCounters, backward WorkCounters)."""
+    import torch
+    settings = settings or NewtonSettings()
+    solver = solver or SolverChoice()
+    ctx = ctx or default_context()
+    n = model.state_size
+    if d_y0.dtype != torch.float64 or d_times.dtype != torch.float64 or not (d_y0.is_cuda and d_times.is_cuda):
+        raise TypeError("gradient_adjoint_device: float64 CUDA tensors expected")
+    if d_y0.dim() != 2 or d_y0.shape[1] != n or d_times.dim() != 2 or d_times.shape[1] != d_y0.shape[0]:
+        raise ShapeMismatch("integrate: y0 shape does not match the model / grid")
+    nb, nt = d_y0.shape[0], d_times.shape[0] - 1
+    if d_states is None:
+        d_states = torch.empty((nt + 1, nb * n), dtype=torch.float64, device=d_y0.device)
+    d_y0, d_times = d_y0.contiguous(), d_times.contiguous()
+    grad = np.zeros(model.params.size)
+    L = C.c_double(0.0)
+    wf, wb, e = abi.CkoWork(), abi.CkoWork(), abi.CkoError()
+    st, sv = settings.c(), solver.c()
+    rc = lib().cko_gradient_adjoint_device(ctx.h, ctx.model(model), C.c_void_p(d_y0.data_ptr()),
+                                           C.c_void_p(d_times.data_ptr()), nb, nt, int(n_chunk), C.byref(st),
+                                           C.byref(sv), C.c_void_p(d_states.data_ptr()), C.byref(L), dptr(grad),
+                                           C.byref(wf), C.byref(wb), C.byref(e))
+    raise_for(rc, e)
+    return L.value, grad, d_states, WorkCounters.from_c(wf), WorkCounters.from_c(wb)
+
+
 def newton_solve_chunk(model: Model, y_start, dy, t_chunk, dt_chunk, settings: NewtonSettings | None = None,
                        solver: SolverChoice | None = None, work: WorkCounters | None = None,
                        chunk_start_step: int = 1, ctx: Context | None = None):

@@ -161,6 +161,8 @@ struct cko_ctx {
   int sms = 0;
   // workspace pool
   Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
+  Buf lpart;       // the last forward's per-CTA sums of y^2 (the fused Frobenius loss)
+  int lpart_n = 0;  // how many (0: the last forward left none)
   Buf h_y0, h_times, h_states, h_dL, h_rhs, h_diag, h_off;  // staging for host-buffer calls
   std::vector<int> iters_host;
   PinBuf pin;
@@ -486,11 +488,13 @@ cko_status prepare_slab(cko_ctx* c, int G, int nb, int nc, int n, bool pcr, Slab
 }
 
 constexpr int kThreads = 256;
+constexpr int kThreadsMax = 1024;  // largest block of any forward kernel (the loss slots)
 
 // Core forward on device buffers (states row 0 must hold y0).
 cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
                         int nc, const cko_newton_settings* st, const cko_solver_choice* sv, const double* d_dy,
-                        cko_work* work, int* iters_out, cko_error* err, const double* d_dts = nullptr) {
+                        cko_work* work, int* iters_out, cko_error* err, const double* d_dts = nullptr,
+                        bool want_loss_part = false) {
   if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: n_chunk must be >= 1");
   if (nt < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: need at least one step");
@@ -557,6 +561,11 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.budget_ns = 60ull * 1000 * 1000 * 1000;
   a.grid = G;
   a.threads = kThreads;
+  c->lpart_n = 0;
+  if (want_loss_part && (v2 || p2)) {  // the loss rides on the residual passes (one partial per CTA)
+    CUDA_TRY(c->lpart.ensure(sizeof(double) * G * (1 + 2 * (size_t)kThreadsMax)));  // + per-thread slots
+    a.loss_part = c->lpart.as<double>();
+  }
   static const char* trace_path = std::getenv("CKO_TRACE");
   Buf tbuf;
   if (trace_path && v2) {
@@ -683,6 +692,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
     return s;
   }
   if (info[3] != n_chunks) return fail(err, CKO_CUDA, "forward kernel stopped after %d of %d chunks", info[3], n_chunks);
+  if (a.loss_part) c->lpart_n = G;
   if (work) {
     std::memset(work, 0, sizeof(*work));
     for (int j = 0; j < n_chunks; ++j) {
@@ -703,7 +713,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
 cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, const double* d_times, int nb,
                         int nt, int nc, const cko_solver_choice* sv, int loss_kind, const double* d_dL,
                         double* loss_out, double* grad_out, cko_work* bwd, cko_error* err,
-                        bool keep_lambda = false) {
+                        bool keep_lambda = false, bool fwd_loss = false) {
   if (m) const_cast<cko_model*>(m)->dm.jstrat = c->jstrat;  // the call's JacobianStrategy
   if (nc < 1) return fail(err, CKO_SHAPE_MISMATCH, "adjoint: n_chunk must be >= 1");
   if (sv->kind < 0 || sv->kind > 2) return fail(err, CKO_ERROR, "unknown solver kind %d", sv->kind);
@@ -748,11 +758,22 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   c->last_launches = 3;
   c->last_gen = (nodep || v2 || p2) ? 2 : 1;
   c->mark(6);
-  if (loss_kind == CKO_LOSS_FROBENIUS) {
+  // Frobenius loss: straight after this call's own forward, from the per-CTA partials the forward left
+  // (formed inside the generation-2 adjoint on one rank, else one small kernel that also sums the group);
+  // otherwise a pass over the trajectory
+  const int lpart_n = c->lpart_n;
+  const bool lpart = fwd_loss && lpart_n > 0 && loss_kind == CKO_LOSS_FROBENIUS;
+  const bool lpart_in_adj = lpart && (v2 || p2) && c->grp.world <= 1;
+  if (lpart && !lpart_in_adj) {
+    CUDA_TRY(launch_loss_final(c->lpart.as<double>(), lpart_n, c->scratch.as<double>(), c->loss.as<double>(),
+                               c->grp, c->gs.as<GridSync>(), c->status.as<unsigned>(), c->stream));
+    c->last_launches += 1;
+  } else if (!lpart && loss_kind == CKO_LOSS_FROBENIUS) {
     CUDA_TRY(launch_loss(d_states, nt, (int)row, c->scratch.as<double>(), c->loss.as<double>(), c->grp,
                          c->gs.as<GridSync>(), c->status.as<unsigned>(), c->stream));
     c->last_launches += 2;
   }
+  c->lpart_n = 0;
   c->mark(7);
   AdjLaunch a{};
   a.m = m->dm;
@@ -760,6 +781,11 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.times = d_times;
   a.dL = loss_kind == CKO_LOSS_USER ? d_dL : nullptr;
   a.loss = loss_kind == CKO_LOSS_USER ? nullptr : c->loss.as<double>();
+  if (lpart_in_adj) {
+    a.loss_part = c->lpart.as<double>();
+    a.loss_nparts = lpart_n;
+    a.loss_out = c->loss.as<double>();
+  }
   a.nb = nb;
   a.nt = nt;
   a.nc = nc;
@@ -1004,6 +1030,28 @@ cko_status cko_be_forward_device(cko_ctx* c, const cko_model* m, const double* d
   return forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, work, nullptr, err);
 }
 
+cko_status cko_gradient_adjoint_device(cko_ctx* c, const cko_model* m, const double* d_y0, const double* d_times,
+                                       int nb, int nt, int nc, const cko_newton_settings* st,
+                                       const cko_solver_choice* sv, double* d_states, double* loss_out,
+                                       double* grad_out, cko_work* fwd, cko_work* bwd, cko_error* err) {
+  if (!c || !m || !d_y0 || !d_times || !d_states || !st || !sv || !grad_out) return fail(err, CKO_ERROR, "null argument");
+  if (nb < 1) return fail(err, CKO_SHAPE_MISMATCH, "integrate: y0 rows != grid batch width");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t row = (size_t)nb * m->dm.n;
+  if (d_states != d_y0)
+    CUDA_TRY(cudaMemcpyAsync(d_states, d_y0, sizeof(double) * row, cudaMemcpyDeviceToDevice, c->stream));
+  if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err, nullptr,
+                                  true))
+    return s;
+  const int fwd_launches = c->last_launches;
+  const double fwd_ms = c->last_ms[0];
+  cko_status s = adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out,
+                              grad_out, bwd, err, false, true);
+  c->last_launches += fwd_launches;  // the step's launches and kernel times, forward included
+  c->last_ms[0] = fwd_ms;
+  return s;
+}
+
 cko_status cko_be_forward(cko_ctx* c, const cko_model* m, const double* y0, const double* times, int nb, int nt,
                           int nc, const cko_newton_settings* st, const cko_solver_choice* sv, double* states_out,
                           cko_traj** traj_out, cko_work* work, cko_error* err) {
@@ -1130,10 +1178,12 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
   CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
   if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
-  if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err)) return s;
+  if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err,
+                                  nullptr, true))
+    return s;
   if (!states_out)
     return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out, grad_out,
-                        bwd, err);
+                        bwd, err, false, true);
   // The trajectory download overlaps the adjoint (both only read d_states): a helper thread copies it on
   // the context's copy stream (a pageable destination blocks the issuing thread, not the adjoint's
   // launches), while this thread runs the adjoint on the compute stream.
@@ -1150,7 +1200,7 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
     if (copy_err == cudaSuccess) copy_err = cudaStreamSynchronize(c->copy_stream);
   });
   cko_status s = adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out,
-                              grad_out, bwd, err);
+                              grad_out, bwd, err, false, true);
   copier.join();
   if (s != CKO_OK) return s;
   if (copy_err != cudaSuccess) return fail(err, CKO_CUDA, "trajectory D2H: %s", cudaGetErrorString(copy_err));

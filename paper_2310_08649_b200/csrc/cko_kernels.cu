@@ -131,6 +131,13 @@ cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, 
   return cudaGetLastError();
 }
 
+// The loss from per-CTA partials the forward left (sum of y^2 per CTA), summed across the group.
+cudaError_t launch_loss_final(const double* part, int nparts, double* scratch, double* loss, const GroupView& g,
+                              GridSync* gs, unsigned* status, cudaStream_t st) {
+  loss_final_kernel<<<1, 256, 0, st>>>(part, nparts, scratch, loss, g, gs, 60ull * 1000 * 1000 * 1000, status);
+  return cudaGetLastError();
+}
+
 __global__ void group_sum_kernel(GroupView g, GridSync* gs, double* v, int cnt, uint64_t budget_ns, unsigned* status) {
   group_sum_block(g, gs, v, cnt, v, budget_ns, status);
 }
@@ -277,8 +284,15 @@ cudaError_t launch_solve(const SolveLaunch& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t vjp_static_mds(const DevModel& m, const double* states, const double* times, const double* wq, int nb,
+                           int nt, double* scratch, cudaStream_t st);
+
 static cudaError_t vjp_dispatch(const DevModel& m, const double* states, const double* times, const double* wq,
                                 int nb, int nt, double* scratch, cudaStream_t st) {
+  if (m.kind == 3) {  // compile-time-sized MDS VJP (n = 4, 20)
+    const cudaError_t e = vjp_static_mds(m, states, times, wq, nb, nt, scratch, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
 #define CALL(N) vjp_run_##N(m, states, times, wq, nb, nt, scratch, st)
   CKO_SWITCH(m.kind, CALL)
 #undef CALL

@@ -45,6 +45,7 @@ struct FwdLaunch {
   int* info;             // [0] status, [1] chunk_start_step, [2] iterations, [3] n_chunks done
   uint64_t budget_ns;
   unsigned long long* trace;  // optional diagnostics (CKO_TRACE): per-row timestamps of CTA 0
+  double* loss_part;      // optional (grid): per-CTA sum of y^2 over rows 1..nt (generation-2 kernels)
   int grid;               // CTAs
   int threads;
 };
@@ -55,6 +56,9 @@ struct AdjLaunch {
   const double* times;   // (nt+1, nb)
   const double* dL;      // optional user dL (nt+1, nb, n); null = Frobenius y / L
   const double* loss;    // device scalar L (Frobenius)
+  const double* loss_part;  // optional: the forward's per-CTA sums of y^2 (loss_nparts of them); the v2 kernel
+  int loss_nparts;          // then forms L itself and CTA 0 stores it to loss_out
+  double* loss_out;
   int nb, nt, nc;
   int solver, n_switch;
   Slab slab;
@@ -113,6 +117,9 @@ inline int pcr2_ws_bound(int n) { return 3 * n * n + 5 * n + 20; }
 // group (world > 1) the sum of squares is summed over ranks first.
 cudaError_t launch_loss(const double* states, int nt, int row, double* scratch, double* loss,
                         const GroupView& g, GridSync* gs, unsigned* status, cudaStream_t st);
+// The same from nparts per-CTA partial sums of y^2 (FwdLaunch::loss_part); scratch >= 1 double.
+cudaError_t launch_loss_final(const double* part, int nparts, double* scratch, double* loss, const GroupView& g,
+                              GridSync* gs, unsigned* status, cudaStream_t st);
 // In-place deterministic sum of v[0..cnt) over the ranks of the group.
 cudaError_t launch_chunk_op(const DevModel& m, int op, const double* ys, const double* dy, const double* t,
                             const double* dt, int c, int nb, double* yyb, double* out, unsigned* flags,

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
   const int T = blockDim.x, tid = threadIdx.x, nb = a.nb;
   __syncthreads();
   int step = 0, chunk = 0;
+  if (a.loss_part) *loss_slot(a) = 0.0;  // Frobenius loss partial: sum y^2 of converged rows (this thread's)
   while (step < a.nt) {
     const int c = min(a.nc, a.nt - step);
     x.step = step;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
     int it = 0;
     // residual staging in the (idle) shared-memory PCR workspace, if it lives there
     const int stage_cap = in_smem ? (int)(dyn_smem_bytes() / 8) - OCS : 0;
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, true, &s_flags);
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, true, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr);
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
       if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
@@ -355,7 +356,7 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
       }
       __syncthreads();
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
-      f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, false, &s_flags) | fl;
+      f = residual2<MS>(a, x, cs, hr, nrm, smem + OCS, stage_cap, false, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr) | fl;
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
       if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
         if (leader) {
@@ -366,12 +367,14 @@ __global__ void __launch_bounds__(512, 1) fwd_pcr2_kernel(FwdLaunch a, int in_sm
         return;
       }
     }
+    if (a.loss_part) loss_slot(a)[0] += loss_slot(a)[1];  // the last residual pass saw the converged iterate
     if (leader) a.iters[chunk] = it;
     step += c;
     ++chunk;
     __syncthreads();
   }
   if (leader) a.info[3] = chunk;
+  if (a.loss_part) fwd_loss_store(a.loss_part, *loss_slot(a));
 }
 
 // ---------------------------------------------------------------------------
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(512, 1) adj_pcr2_kernel(AdjLaunch a, int in_sm
   lane_range(a.nb, lb0, L);
   const int T = blockDim.x, tid = threadIdx.x, nb = a.nb;
   const size_t row = (size_t)nb * N;
-  const double Lval = a.loss ? *a.loss : 0.0;
+  const double Lval = adj_loss_value(a);
   double* lam = smem + OCS;  // (L, N) carry
   const int olam = OCS + ((L * N + 1) / 2) * 2;
   for (int i = tid; i < L * N; i += T) lam[i] = 0.0;

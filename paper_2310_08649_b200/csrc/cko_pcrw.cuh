@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
   const int stage_cap = kPcrwWarps * WSlot<N>::STRIDE;  // residual staging in the idle sweep slots
   __syncthreads();
   int step = 0, chunk = 0;
+  if (a.loss_part) *loss_slot(a) = 0.0;  // Frobenius loss partial: sum y^2 of converged rows (this thread's)
   while (step < a.nt) {
     const int c = min(a.nc, a.nt - step);
     x.step = step;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
     }
     __syncthreads();
     int it = 0;
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, slots, stage_cap, true, &s_flags);
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, slots, stage_cap, true, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr);
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
     if (f & (FLAG_TIMEOUT | FLAG_NON_FINITE)) {
       if (leader) a.info[0] = (f & FLAG_TIMEOUT) ? 4 : 2, a.info[1] = step + 1, a.info[2] = 0;
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
       __syncthreads();
       }  // lane tiles
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
-      f = residual2<MS>(a, x, cs, hr, nrm, slots, stage_cap, false, &s_flags) | fl;
+      f = residual2<MS>(a, x, cs, hr, nrm, slots, stage_cap, false, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr) | fl;
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
       if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
         if (leader) {
@@ -369,12 +370,14 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
         return;
       }
     }
+    if (a.loss_part) loss_slot(a)[0] += loss_slot(a)[1];  // the last residual pass saw the converged iterate
     if (leader) a.iters[chunk] = it;
     step += c;
     ++chunk;
     __syncthreads();
   }
   if (leader) a.info[3] = chunk;
+  if (a.loss_part) fwd_loss_store(a.loss_part, *loss_slot(a));
 }
 
 // ---------------------------------------------------------------------------
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) adj_pcrw_kernel(AdjLaunch 
   lane_range(a.nb, lb0, L);
   const int T = blockDim.x, tid = threadIdx.x, nb = a.nb, warp = tid >> 5, lane = tid & 31;
   const size_t row = (size_t)nb * N;
-  const double Lval = a.loss ? *a.loss : 0.0;
+  const double Lval = adj_loss_value(a);
   double* ws = align16(a.slab.base + (size_t)blockIdx.x * a.slab.doubles);
   double* lam = a.lambda + (size_t)lb0 * N;  // the carry (global, this CTA's lanes)
   for (int i = tid; i < L * N; i += T) lam[i] = 0.0;

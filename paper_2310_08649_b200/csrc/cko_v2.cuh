@@ -828,10 +828,13 @@ __device__ __forceinline__ unsigned dyn_smem_bytes() {
 // Residual + lane norms for all c x L points of this CTA (rate_residual_norms,
 // integrate.cpp:64-95). The chunk's iterate yy_k lives in its final place,
 // trajectory row step + 1 + k, so yy_{-1} = y_start is row `step`.
+// *ssq (if given): this thread's sum of y_i^2 over the points it evaluated (its
+// share of the Frobenius loss of the chunk's rows once the chunk converges).
 template <class MS>
 __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double* cs, double* hr, double* nrm,
-                              double* stage, int cap, bool first, unsigned* s_flags,
+                              double* stage, int cap, bool first, unsigned* s_flags, double* ssq,
                               unsigned long long* rtr = nullptr) {
+  double sq = 0.0;
   constexpr int N = MS::N;
   const int nb = a.nb, L = x.L, LN = L * N, P = x.c * L;
   // Staged in shared memory (the idle record ring): the CTA's lanes of one
@@ -862,6 +865,7 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
         const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
         o[i] = v;
         s = xadd(s, xmul(v, v));
+        sq += y[i] * y[i];
       }
       nrm[p] = s;
     }
@@ -912,6 +916,7 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
           const double v = xsub(xsub(y[i], ym[i]), xmul(h[i], dt));
           o[i] = v;
           s = xadd(s, xmul(v, v));
+          sq += y[i] * y[i];
         }
         nrm[(k0 + kk) * L + lb] = s;
       }
@@ -929,6 +934,7 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
       __syncthreads();
     }
   }
+  if (ssq) *ssq = sq;
   if (threadIdx.x == 0) *s_flags = 0;
   if (rtr) rtr[0] = globaltimer_ns();
   __syncthreads();
@@ -954,6 +960,48 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
   if (rtr) rtr[2] = globaltimer_ns();
   __syncthreads();
   return *s_flags;
+}
+
+// This thread's [committed, pending] sums of y^2 (global, after the per-CTA
+// partials: nothing stays live in registers through the factorisations).
+__device__ __forceinline__ double* loss_slot(const FwdLaunch& a) {
+  return a.loss_part + a.grid + 2 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+}
+
+// The CTA's Frobenius-loss partial (sum of y^2 over its converged rows) in a
+// fixed order: warp sums, then warp 0 over the warps. The whole CTA calls it.
+__device__ inline void fwd_loss_store(double* loss_part, double v) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[w];
+    loss_part[blockIdx.x] = s;
+  }
+}
+
+// The Frobenius loss L for the adjoint's dL/dy = y / L: the device scalar, or —
+// straight after the forward that left per-CTA sums of y^2 — their sum (warp 0,
+// fixed order; every CTA forms the same value) and CTA 0 publishes it. The whole
+// CTA calls it.
+__device__ inline double adj_loss_value(const AdjLaunch& a) {
+  if (!a.loss_part) return a.loss ? *a.loss : 0.0;
+  __shared__ double s_L;
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < a.loss_nparts; i += 32) v += a.loss_part[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) {
+      s_L = sqrt(v);
+      if (blockIdx.x == 0) *a.loss_out = s_L;
+    }
+  }
+  __syncthreads();
+  return s_L;
 }
 
 // One Newton iteration over the rows of one lane tile (integrate.cpp:208-231).
@@ -1175,6 +1223,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
   int step = 0, chunk = 0;
+  if (a.loss_part) *loss_slot(a) = 0.0;  // Frobenius loss partial: sum y^2 of converged rows (this thread's)
   while (step < a.nt) {
     const int c = min(a.nc, a.nt - step);
     x.step = step;
@@ -1201,7 +1250,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
                                   ? a.trace + 64 + 8 * (size_t)min(a.nc, a.nt) + 8 * blockIdx.x : nullptr;
     if (ctr) ctr[0] = globaltimer_ns();
     if (ktr) ktr[0] = globaltimer_ns();
-    unsigned f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, true, &s_flags, ktr ? ktr + 11 : nullptr);
+    unsigned f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, true, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr, ktr ? ktr + 11 : nullptr);
     if (ktr) ktr[1] = globaltimer_ns();
     if (ctr) ctr[1] = globaltimer_ns();
     f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
@@ -1224,7 +1273,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
       const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
       if (ktr && it < 4) ktr[3 + 3 * (it - 1)] = globaltimer_ns();
       if (ctr && it == 1) ctr[3] = globaltimer_ns();
-      f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, false, &s_flags) | fl;
+      f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, false, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr) | fl;
       if (ctr && it == 1) ctr[4] = globaltimer_ns();
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
       if (ctr && it == 1) ctr[5] = globaltimer_ns();
@@ -1238,12 +1287,14 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
         return;
       }
     }
+    if (a.loss_part) loss_slot(a)[0] += loss_slot(a)[1];  // the last residual pass saw the converged iterate
     if (leader) a.iters[chunk] = it;
     step += c;
     ++chunk;
     __syncthreads();
   }
   if (leader) a.info[3] = chunk;
+  if (a.loss_part) fwd_loss_store(a.loss_part, *loss_slot(a));
 }
 
 // ---------------------------------------------------------------------------
@@ -1485,7 +1536,7 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
   MS::load_consts(a.m, cs);
   int lb0, L;
   lane_range(a.nb, lb0, L);
-  const double Lval = a.loss ? *a.loss : 0.0;
+  const double Lval = adj_loss_value(a);
   const int consumer = threadIdx.x >> 5 == 0;
   const int lane = threadIdx.x & 31;
   for (int t0 = 0; t0 < L; t0 += sh.LT) {
