@@ -14,7 +14,9 @@
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
+#include <cuda.h>
 #include <new>
+#include <numeric>
 #include <thread>
 #include <vector>
 
@@ -162,6 +164,11 @@ struct cko_ctx {
   // workspace pool
   Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
   Buf lpart;       // the last forward's per-CTA sums of y^2 (the fused Frobenius loss)
+  Buf feed;        // streamed time grid: rows resident (tag + rows, written by the copy stream)
+  unsigned long long feed_calls = 0;
+  const unsigned long long* feed_ready = nullptr;  // set for the next forward_core only
+  unsigned long long feed_tag = 0;
+  cudaEvent_t times_done = nullptr;
   int lpart_n = 0;  // how many (0: the last forward left none)
   Buf h_y0, h_times, h_states, h_dL, h_rhs, h_diag, h_off;  // staging for host-buffer calls
   std::vector<int> iters_host;
@@ -491,6 +498,49 @@ constexpr int kThreads = 256;
 constexpr int kThreadsMax = 1024;  // largest block of any forward kernel (the loss slots)
 
 // Core forward on device buffers (states row 0 must hold y0).
+// Whether forward_core runs a generation-2 forward (the kernels that can wait on a streamed grid):
+// the same decision forward_core makes for a call without explicit step sizes.
+bool fwd_streams_times(cko_ctx* c, const cko_model* m, const cko_solver_choice* sv) {
+  if (c->jstrat != 0 || c->kernel_gen < 2 || sv->kind < 0 || sv->kind > 2) return false;
+  const int n = m->dm.n;
+  if (sv->kind != CKO_SOLVER_THOMAS) return launch_forward_pcr2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+  return !node_fast_path(m->dm) && launch_forward_v2(m->dm.kind, n, nullptr, c->stream) == cudaSuccess;
+}
+
+// First flat index e >= nb of a host grid (nt+1, nb) with !(t[e] > t[e - nb]), or -1 (grid_check_kernel).
+long long first_bad_time(const double* t, int nt, int nb) {
+  const long long total = (long long)nb * (nt + 1);
+  for (long long e = nb; e < total; ++e)
+    if (!(t[e] > t[e - nb])) return e;
+  return -1;
+}
+
+// cuStreamWriteValue64 (driver API, through the runtime's entry-point query), or null when the driver or
+// the device lacks 64-bit stream memory operations.
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WriteValue64Fn write_value64(int device) {
+  static WriteValue64Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<WriteValue64Fn>(f);
+  }();
+  using AttrFn = CUresult (*)(int*, CUdevice_attribute, CUdevice);
+  static AttrFn attr = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<AttrFn>(f);
+  }();
+  int ok = 0;
+  if (!fn || !attr || attr(&ok, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, device) != CUDA_SUCCESS) ok = 0;
+  return ok ? fn : nullptr;
+}
+
 cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const double* d_times, int nb, int nt,
                         int nc, const cko_newton_settings* st, const cko_solver_choice* sv, const double* d_dy,
                         cko_work* work, int* iters_out, cko_error* err, const double* d_dts = nullptr,
@@ -561,6 +611,12 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
   a.budget_ns = 60ull * 1000 * 1000 * 1000;
   a.grid = G;
   a.threads = kThreads;
+  if (c->feed_ready) {  // the caller streams the grid only to the generation-2 kernels (fwd_streams_times)
+    a.times_ready = c->feed_ready;
+    a.times_tag = c->feed_tag;
+    c->feed_ready = nullptr;
+    if (!(v2 || p2)) return fail(err, CKO_ERROR, "internal: streamed time grid for a kernel that cannot wait on it");
+  }
   c->lpart_n = 0;
   if (want_loss_part && (v2 || p2)) {  // the loss rides on the residual passes (one partial per CTA)
     CUDA_TRY(c->lpart.ensure(sizeof(double) * G * (1 + 2 * (size_t)kThreadsMax)));  // + per-thread slots
@@ -1175,12 +1231,66 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
   CUDA_TRY(c->h_times.ensure(sizeof(double) * (size_t)nb * (nt + 1)));
   double* d_states = c->h_states.as<double>();
   double* d_times = c->h_times.as<double>();
-  CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(d_states, y0, sizeof(double) * row, cudaMemcpyHostToDevice, c->stream));
-  if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
-  if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err,
-                                  nullptr, true))
-    return s;
+  static const bool no_stream = [] {
+    const char* v = std::getenv("CKO_NO_TIME_STREAM");  // A/B: upload the whole grid before the forward
+    return v && v[0] == '1';
+  }();
+  const int nc_eff = nc < nt ? nc : nt;
+  if (no_stream || nc < 1 || nt < 4 * nc_eff || !write_value64(c->device) || !fwd_streams_times(c, m, sv)) {
+    CUDA_TRY(cudaMemcpyAsync(d_times, times, sizeof(double) * (size_t)nb * (nt + 1), cudaMemcpyHostToDevice,
+                             c->stream));
+    if (cko_status s = check_grid_device(c, d_times, nt, nb, err)) return s;
+    if (cko_status s = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err,
+                                    nullptr, true))
+      return s;
+  } else {
+    // The grid streams in while the forward runs: the first chunk's rows, then pieces of several chunks, on
+    // the copy stream, each followed by a stream write of the rows now resident
+    // (the kernels wait per chunk, wait_times_rows). The grid check runs on the host meanwhile; a bad grid
+    // discards the forward and reports the same first index as grid_check_kernel.
+    if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (!c->times_done) CUDA_TRY(cudaEventCreateWithFlags(&c->times_done, cudaEventDisableTiming));
+    CUDA_TRY(c->feed.ensure(sizeof(unsigned long long)));
+    const unsigned long long tag = (++c->feed_calls) << 32;
+    const int ra = 16 / std::gcd(nb, 16);  // rows per 128 bytes: piece boundaries on cache-line boundaries
+    auto up = [&](long long r) { return std::min<long long>(nt + 1, (r + ra - 1) / ra * ra); };
+    const long long r0 = up(nc_eff + 1);
+    const long long piece = std::max<long long>(up(4LL * nc_eff), (4LL << 20) / (8LL * nb) / ra * ra);
+    const CUdeviceptr flag = reinterpret_cast<CUdeviceptr>(c->feed.p);
+    const WriteValue64Fn wv = write_value64(c->device);
+    long long bad = -1;
+    std::thread checker([&] { bad = first_bad_time(times, nt, nb); });
+    cudaError_t feed_err = cudaSuccess;
+    std::thread feeder([&] {  // a pageable grid blocks the issuing thread, not the forward's launch
+      feed_err = cudaSetDevice(c->device);
+      // one stream carries every piece and its write: the resident-row count only grows
+      for (long long r = 0; feed_err == cudaSuccess && r < nt + 1; r = r == 0 ? r0 : r + piece) {
+        const long long e = r == 0 ? r0 : std::min<long long>(nt + 1, r + piece);
+        feed_err = cudaMemcpyAsync(d_times + (size_t)r * nb, times + (size_t)r * nb, sizeof(double) * nb * (e - r),
+                                   cudaMemcpyHostToDevice, c->copy_stream);
+        if (feed_err == cudaSuccess &&
+            wv(reinterpret_cast<CUstream>(c->copy_stream), flag, tag + e, 0) != CUDA_SUCCESS)
+          feed_err = cudaErrorUnknown;
+      }
+      if (feed_err == cudaSuccess) feed_err = cudaEventRecord(c->times_done, c->copy_stream);
+    });
+    c->feed_ready = reinterpret_cast<const unsigned long long*>(c->feed.p);
+    c->feed_tag = tag;
+    const cko_status fs = forward_core(c, m, d_states, d_times, nb, nt, nc, st, sv, nullptr, fwd, nullptr, err,
+                                       nullptr, true);
+    c->feed_ready = nullptr;
+    feeder.join();
+    checker.join();
+    if (feed_err == cudaSuccess) feed_err = cudaStreamWaitEvent(c->stream, c->times_done, 0);
+    if (feed_err == cudaSuccess) feed_err = cudaStreamSynchronize(c->copy_stream);
+    if (bad >= 0) {
+      const int i = (int)(bad / nb), b = (int)(bad % nb);
+      return fail(err, CKO_INVALID_TIME_GRID, "time grid must be strictly increasing (step %d, batch %d)", i, b);
+    }
+    if (feed_err != cudaSuccess) return fail(err, CKO_CUDA, "time grid upload: %s", cudaGetErrorString(feed_err));
+    if (fs != CKO_OK) return fs;
+  }
   if (!states_out)
     return adjoint_core(c, m, d_states, d_times, nb, nt, nc, sv, CKO_LOSS_FROBENIUS, nullptr, loss_out, grad_out,
                         bwd, err, false, true);

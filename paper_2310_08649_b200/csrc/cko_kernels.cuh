@@ -46,6 +46,10 @@ struct FwdLaunch {
   uint64_t budget_ns;
   unsigned long long* trace;  // optional diagnostics (CKO_TRACE): per-row timestamps of CTA 0
   double* loss_part;      // optional (grid): per-CTA sum of y^2 over rows 1..nt (generation-2 kernels)
+  // optional streamed time grid (generation-2 kernels): rows [0, R) of `times` are resident once
+  // *times_ready >= times_tag + R (written by the copy stream after each piece)
+  const unsigned long long* times_ready;
+  unsigned long long times_tag;
   int grid;               // CTAs
   int threads;
 };

@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(32 * kPcrwWarps, 1) fwd_pcrw_kernel(FwdLaunch 
   if (a.loss_part) *loss_slot(a) = 0.0;  // Frobenius loss partial: sum y^2 of converged rows (this thread's)
   while (step < a.nt) {
     const int c = min(a.nc, a.nt - step);
+    if (a.times_ready && !wait_times_rows(a, step + c + 1)) {  // this chunk's rows of the streamed grid
+      if (leader) a.info[0] = 4, a.info[1] = step + 1, a.info[2] = 0;
+      return;
+    }
     x.step = step;
     x.c = c;
     for (int p = tid; p < c * x.L; p += T) {  // initial iterate: every row at y_start

@@ -962,6 +962,32 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
   return *s_flags;
 }
 
+// Streamed time grid: block until rows [0, rows) of a.times have landed (the
+// host uploads the grid in pieces on a copy stream while the forward runs; the
+// piece boundaries are 128-byte aligned, so no cache line straddles a piece).
+// The whole CTA calls it; false on timeout.
+__device__ inline bool wait_times_rows(const FwdLaunch& a, int rows) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    const unsigned long long want = a.times_tag + (unsigned long long)rows;
+    const uint64_t t0 = globaltimer_ns();
+    int ok = 1;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.times_ready) : "memory");
+      if (v >= want) break;
+      if (globaltimer_ns() - t0 > a.budget_ns) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(256);
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
 // This thread's [committed, pending] sums of y^2 (global, after the per-CTA
 // partials: nothing stays live in registers through the factorisations).
 __device__ __forceinline__ double* loss_slot(const FwdLaunch& a) {
@@ -1226,6 +1252,10 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   if (a.loss_part) *loss_slot(a) = 0.0;  // Frobenius loss partial: sum y^2 of converged rows (this thread's)
   while (step < a.nt) {
     const int c = min(a.nc, a.nt - step);
+    if (a.times_ready && !wait_times_rows(a, step + c + 1)) {  // this chunk's rows of the streamed grid
+      if (leader) a.info[0] = 4, a.info[1] = step + 1, a.info[2] = 0;
+      return;
+    }
     x.step = step;
     x.c = c;
     for (int p = threadIdx.x; p < c * x.L; p += blockDim.x) {  // initial iterate: every row at y_start
