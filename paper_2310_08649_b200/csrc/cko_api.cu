@@ -8,6 +8,7 @@
 // types (errors.hpp:9-69). No CPU fallback exists: without a usable CUDA
 // device every entry point returns CKO_CUDA.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -165,7 +166,6 @@ struct cko_ctx {
   Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
   Buf lpart;       // the last forward's per-CTA sums of y^2 (the fused Frobenius loss)
   Buf feed;        // streamed time grid: rows resident (tag + rows, written by the copy stream)
-  unsigned long long feed_calls = 0;
   const unsigned long long* feed_ready = nullptr;  // set for the next forward_core only
   unsigned long long feed_tag = 0;
   cudaEvent_t times_done = nullptr;
@@ -1251,8 +1251,14 @@ cko_status cko_gradient_adjoint(cko_ctx* c, const cko_model* m, const double* y0
     // discards the forward and reports the same first index as grid_check_kernel.
     if (!c->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     if (!c->times_done) CUDA_TRY(cudaEventCreateWithFlags(&c->times_done, cudaEventDisableTiming));
-    CUDA_TRY(c->feed.ensure(sizeof(unsigned long long)));
-    const unsigned long long tag = (++c->feed_calls) << 32;
+    if (!c->feed.p) {  // a recycled allocation may hold another context's count: start from zero
+      CUDA_TRY(c->feed.ensure(sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemset(c->feed.p, 0, sizeof(unsigned long long)));
+      CUDA_TRY(cudaDeviceSynchronize());
+    }
+    // tags grow process-wide, so a stale count from any earlier call can never satisfy this call's waits
+    static std::atomic<unsigned long long> feed_calls{0};
+    const unsigned long long tag = (++feed_calls) << 32;
     const int ra = 16 / std::gcd(nb, 16);  // rows per 128 bytes: piece boundaries on cache-line boundaries
     auto up = [&](long long r) { return std::min<long long>(nt + 1, (r + ra - 1) / ra * ra); };
     const long long r0 = up(nc_eff + 1);
