@@ -159,7 +159,8 @@ cudaError_t launch_group_sum(const GroupView& g, GridSync* gs, double* v, int cn
 __global__ void vjp_final_kernel(const double* part, int nblk, int np, double* grad) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < np; j += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int q = 0; q < nblk; ++q) s += part[(size_t)q * np + j];
+#pragma unroll 16
+    for (int q = 0; q < nblk; ++q) s += part[(size_t)q * np + j];  // loads in flight, sums in row order
     grad[j] = s;
   }
 }
