@@ -53,6 +53,22 @@ struct MdsS {
     for (int e = threadIdx.x; e < 4 * N; e += blockDim.x)
       cs[ZOFF + e] = (e == N - 1 || e == 2 * N + N) ? 1.0 : -0.0;
   }
+  // (J^T lambda)_i over the structural nonzeros of column i of J (jac_row's entries), ascending j: the
+  // dense j-ascending multiply-add over all N entries adds only exact zeros besides these.
+  __device__ static double jt_lambda(const double* cs, int i, const double* lm) {
+    // branch-free (the lanes of a group hold different columns): absent neighbours add exact zeros
+    const bool vel = i >= NU;
+    const int k = vel ? i - NU : i;
+    const double* c = cs + (vel ? NU : 0);
+    const double lo = k > 0 ? -c[k] : 0.0, hi = k + 1 < NU ? -c[k + 1] : 0.0;
+    const double mid = (0.0 + (k > 0 ? c[k] : 0.0)) + (k + 1 < NU ? c[k + 1] : 0.0);
+    double tmp = 0.0;
+    if (vel) tmp += 1.0 * lm[k];
+    tmp += lo * lm[NU + (k > 0 ? k - 1 : 0)];
+    tmp += mid * lm[NU + k];
+    tmp += hi * lm[NU + (k + 1 < NU ? k + 1 : k)];
+    return tmp;
+  }
   // row i of I (1 on the diagonal, -0.0 elsewhere), 16-byte aligned
   __device__ static const double* unit_row(const double* cs, int i) {
     const int s = N - 1 - i;

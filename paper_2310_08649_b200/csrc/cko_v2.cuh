@@ -104,6 +104,20 @@ constexpr int kMaxWs = 3;     // producer warps per slot
 #define CKO_INV_MAX_LANES 2  // knob: explicit-inverse records up to this many lanes per CTA (0: never)
 #endif
 constexpr int kInvMaxLanes = CKO_INV_MAX_LANES;
+#ifndef CKO_ADJ_VEC_W
+#define CKO_ADJ_VEC_W 1  // adjoint consumer: weights as 16-byte streaming stores (measured: adjoint 24.6 -> 24.1 ms)
+#endif
+constexpr bool kAdjVecW = CKO_ADJ_VEC_W;
+#ifndef CKO_FWD_EARLY_LOADS
+#define CKO_FWD_EARLY_LOADS 2  // forward producers request the point's iterate / residual (1), and times (2),
+#endif                         // before the slot wait
+constexpr int kFwdEarlyLoads = CKO_FWD_EARLY_LOADS;
+#ifndef CKO_ADJ_LEAN_RHS
+#define CKO_ADJ_LEAN_RHS 12  // adjoint producers, bit mask: 1 sparse J^T lambda, 2 y / L by reciprocal, 4 y loads first,
+                             // 8 times before the slot wait, 16 y before the slot wait
+                             // (measured adjoint ms: none 24.07, 1: 24.39, 2: 24.38, 4: 23.28, 7: 23.71, 8: 25.2, 12: 22.75)
+#endif
+constexpr int kAdjLeanRhs = CKO_ADJ_LEAN_RHS;
 
 // Shared-memory record of one factored point (doubles): the LU factors in
 // the reference's row order (row-major), 1/U_ii, rhs (residual / adjoint
@@ -136,6 +150,24 @@ template <class MS>
 struct HasConstJac<MS, std::void_t<decltype(MS::kConstJac)>> {
   static constexpr bool value = MS::kConstJac;
 };
+
+// Models with a structural-nonzero J^T lambda (MdsS::jt_lambda).
+template <class MS, class = void>
+struct HasJtLambda {
+  static constexpr bool value = false;
+};
+template <class MS>
+struct HasJtLambda<MS, std::void_t<decltype(&MS::jt_lambda)>> {
+  static constexpr bool value = true;
+};
+
+// y / x from r = RN(1 / x): q = y r and one remainder correction (Markstein), the correctly rounded
+// quotient for finite operands away from the overflow / underflow ranges — y / x without the divide
+// sequence.
+__device__ __forceinline__ double div_rn(double y, double x, double r) {
+  const double q = y * r;
+  return fma(fma(-x, q, y), r, q);
+}
 
 // Models that build M row by row kind in the 10-lane group layout (MdsS).
 template <class MS, class = void>
@@ -1064,13 +1096,33 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
       double* rec = recs + (size_t)(q * RS + gi) * kStride;
       unsigned long long* tr = (tr0 && js < x.c) ? tr0 + js * 8 : nullptr;  // slot js: tr[js * 8 + 0..3]
       if (tr) tr[0] = globaltimer_ns();
+      // the point's iterate and residual entries (global) are requested before the slot wait: their
+      // latency overlaps it and the row build
+      [[maybe_unused]] double ye[Gm::R], re[Gm::R];
+      if constexpr (kFwdEarlyLoads >= 1) {
+        const double* yrow = a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N;
+        const double* rrow = hr + (size_t)(k * x.L + lb) * N;
+#pragma unroll
+        for (int q2 = 0; q2 < Gm::R; ++q2) {
+          const int i = gl + q2 * Gm::G;
+          ye[q2] = i < N ? yrow[i] : 0.0;
+          re[q2] = i < N ? rrow[i] : 0.0;
+        }
+      }
+      double t, dt;
+      if constexpr (kFwdEarlyLoads >= 2) {  // the step size before the slot wait too
+        t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+        dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      }
       if (js >= Q) bar_sync(1 + Q + q, nthr);
       if (tr) tr[1] = globaltimer_ns();
-      const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
-      const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      if constexpr (kFwdEarlyLoads < 2) {
+        t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+        dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      }
       double y[N];
       load_vec<N>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N, y);
-      const double* r = hr + (size_t)(k * x.L + lb) * N;
+      [[maybe_unused]] const double* r = hr + (size_t)(k * x.L + lb) * N;
       const double ndt = -dt;
       auto build = [&](double (&m)[Gm::R][N]) {
 #pragma unroll
@@ -1092,8 +1144,13 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
                 if (j == i) m[q][j] = xadd(m[q][j], 1.0);
               }
             }
-            rec[Rec<N>::Y + i] = a.states[(size_t)(x.step + 1 + k) * x.row + (size_t)b * N + i];
-            rec[Rec<N>::RHS + i] = r[i];
+            if constexpr (kFwdEarlyLoads >= 1) {
+              rec[Rec<N>::Y + i] = ye[q];
+              rec[Rec<N>::RHS + i] = re[q];
+            } else {
+              rec[Rec<N>::Y + i] = a.states[(size_t)(x.step + 1 + k) * x.row + (size_t)b * N + i];
+              rec[Rec<N>::RHS + i] = r[i];
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < N; ++j) m[q][j] = 0.0;
@@ -1347,6 +1404,8 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   const int nthr = 32 * (Ws + 1);
   const int nb = a.nb;
   const size_t row = (size_t)nb * N;
+  const double rL = Lval > 0.0 ? 1.0 / Lval : 0.0;  // y / L by div_rn
+  (void)rL;
   const int pw = producer_of(warp);
   if (pw >= 0 && pw < S * Ws) {
     const int s = pw / Ws, sw = pw % Ws;
@@ -1367,16 +1426,77 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
       const int b = lb0 + t0 + ltc;
       const double* lm = lam + (size_t)ltc * N;
       double* rec = recs + (size_t)(q * RS + gi) * kStride;
-      if (js >= Q) bar_sync(1 + Q + q, nthr);
       const int m = step_hi - r;
-      const double t = a.times[(size_t)m * nb + b];
-      const double dt = t - a.times[(size_t)(m - 1) * nb + b];
+      // (8) the point's times, (16) its y (or dL) entries, requested before the slot wait
+      [[maybe_unused]] double yq8[Gm::R];
+      double t, dt;
+      if constexpr ((kAdjLeanRhs & 16) != 0) {  // (16) the y entries too
+#pragma unroll
+        for (int q2 = 0; q2 < Gm::R; ++q2) {
+          const int i = gl + q2 * Gm::G;
+          yq8[q2] = i < N ? (a.dL ? a.dL : a.states)[(size_t)m * row + (size_t)b * N + i] : 0.0;
+        }
+      }
+      if constexpr ((kAdjLeanRhs & 8) != 0) {
+        t = a.times[(size_t)m * nb + b];
+        dt = t - a.times[(size_t)(m - 1) * nb + b];
+      }
+      if (js >= Q) bar_sync(1 + Q + q, nthr);
+      if constexpr ((kAdjLeanRhs & 8) == 0) {
+        t = a.times[(size_t)m * nb + b];
+        dt = t - a.times[(size_t)(m - 1) * nb + b];
+      }
       double y[N];
       load_vec<N>(a.states + (size_t)m * row + (size_t)b * N, y);
       // J rows into the record (scratch), then read back transposed
       auto build = [&](double (&mt)[Gm::R][N]) {
         if constexpr (HasConstJac<MS>::value) {  // J^T rows straight from shared memory
           const double ndt = -dt;
+          if constexpr (kAdjLeanRhs != 0 && HasJtLambda<MS>::value) {
+            double yq[Gm::R];  // (4) the point's y (or user dL) entries first: latency under the row build
+            if constexpr ((kAdjLeanRhs & 16) != 0) {
+#pragma unroll
+              for (int q = 0; q < Gm::R; ++q) yq[q] = yq8[q];
+            } else if constexpr ((kAdjLeanRhs & 4) != 0) {
+#pragma unroll
+              for (int q = 0; q < Gm::R; ++q) {
+                const int i = gl + q * Gm::G;
+                yq[q] = i < N ? (a.dL ? a.dL : a.states)[(size_t)m * row + (size_t)b * N + i] : 0.0;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < Gm::R; ++q) {
+              const int i = gl + q * Gm::G;
+              if (i < N) {
+                const double* JTr = cs + MS::JTOFF + i * N;  // J[j][i], j = 0 .. N-1
+                const double* Er = MS::unit_row(cs, i);
+                double tmp = 0.0;  // (J^T lambda)_i (gemv_transpose)
+                if constexpr ((kAdjLeanRhs & 1) != 0) {
+#pragma unroll
+                  for (int j = 0; j < N; ++j) mt[q][j] = xadd(xmul(ndt, JTr[j]), Er[j]);
+                  tmp = MS::jt_lambda(cs, i, lm);  // (1) structural nonzeros only: the dense sum's value
+                } else {
+#pragma unroll
+                  for (int j = 0; j < N; ++j) {
+                    const double x = JTr[j];
+                    tmp += x * lm[j];
+                    mt[q][j] = xadd(xmul(ndt, x), Er[j]);
+                  }
+                }
+                if constexpr ((kAdjLeanRhs & 20) == 0)
+                  yq[q] = (a.dL ? a.dL : a.states)[(size_t)m * row + (size_t)b * N + i];
+                double dl;
+                if constexpr ((kAdjLeanRhs & 2) != 0)  // (2) y / L from the reciprocal, one correction
+                  dl = a.dL ? yq[q] : (Lval > 0.0 ? div_rn(yq[q], Lval, rL) : 0.0);
+                else
+                  dl = a.dL ? yq[q] : (Lval > 0.0 ? yq[q] / Lval : 0.0);
+                rec[Rec<N>::RHS + i] = dl + dt * tmp;
+              } else {
+#pragma unroll
+                for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
+              }
+            }
+          } else {
 #pragma unroll
           for (int q = 0; q < Gm::R; ++q) {
             const int i = gl + q * Gm::G;
@@ -1397,6 +1517,7 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
 #pragma unroll
               for (int j = 0; j < N; ++j) mt[q][j] = 0.0;
             }
+          }
           }
           if (gl == 0) rec[Rec<N>::DT] = dt;
         } else {
@@ -1542,8 +1663,16 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
         const double dt = rec[Rec<N>::DT];
         lu_solve_rec<N>(rec, vs, d);
         double* w = a.wq + (size_t)m * row + (size_t)b * N;
+        if constexpr (kAdjVecW && N % 2 == 0) {  // 16-byte streaming stores (rows of an even N stay aligned)
 #pragma unroll
-        for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
+          for (int i = 0; i < N; i += 2) {
+            const double2 l2 = *reinterpret_cast<const double2*>(lc + i);
+            __stcs(reinterpret_cast<double2*>(w + i), make_double2((l2.x + d[i]) * dt, (l2.y + d[i + 1]) * dt));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) w[i] = (lc[i] + d[i]) * dt;
+        }
       }
       ring.release(r);
     }
