@@ -4,7 +4,7 @@
 # the n = 20 PCR kernels (C2, short grid). Summaries are written on the box (the .ncu-rep files are too
 # large to travel back and are deleted): gpurun_out/r2_*.
 mkdir -p gpurun_out
-T=r2
+T=${TAG:-r2}
 timeout 1200 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${T}_launches.csv python bench.py --steps 1 --warmup 1 \
