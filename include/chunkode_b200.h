@@ -324,6 +324,19 @@ int cko_ctx_last_launches(cko_ctx* ctx);
  * cko_ctx_kernel_generation_used reports what the last forward / adjoint ran. */
 cko_status cko_ctx_set_kernel_generation(cko_ctx* ctx, int gen);
 int cko_ctx_kernel_generation_used(cko_ctx* ctx);
+/* Structured-record Thomas kernels (generation 2, models whose block
+ * M = I - dt J is [I B; C D] with B, C diagonal bands and D tridiagonal: the
+ * mass-damper-spring chain). On by default; they reproduce lu_factor_block /
+ * lu_solve_vec (linalg.cpp:13-60) whenever the reference would not exchange
+ * rows, and hand any other block (pivoting, singular, non-finite) back to the
+ * group-LU kernels by re-running the call. cko_ctx_structured_used returns
+ * the CKO_SP_* bits of the last forward / adjoint call. */
+#define CKO_SP_FWD 1           /* the forward ran on the structured kernels */
+#define CKO_SP_ADJ 2           /* the adjoint ran on the structured kernels */
+#define CKO_SP_FWD_FALLBACK 4  /* the forward was re-run on the group-LU kernels */
+#define CKO_SP_ADJ_FALLBACK 8  /* the adjoint was re-run on the group-LU kernels */
+cko_status cko_ctx_set_structured(cko_ctx* ctx, int on);
+int cko_ctx_structured_used(cko_ctx* ctx);
 /* JacobianStrategy of the context's following calls (default analytic). */
 cko_status cko_ctx_set_jacobian_strategy(cko_ctx* ctx, int strategy);
 /* FP64 FMA-pipe throughput probe (dependent-chain-free DFMA stream over all

@@ -67,6 +67,8 @@ def lib() -> C.CDLL:
         "cko_probe_fp64_tflops": ([vp, dp, P(E)], C.c_int),
         "cko_ctx_set_kernel_generation": ([vp, C.c_int], C.c_int),
         "cko_ctx_kernel_generation_used": ([vp], C.c_int),
+        "cko_ctx_set_structured": ([vp, C.c_int], C.c_int),
+        "cko_ctx_structured_used": ([vp], C.c_int),
         "cko_newton_solve_chunk": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, P(N), P(S), C.c_int, P(C.c_int), P(W),
                                     P(E)], C.c_int),
         "cko_chunk_residual": ([vp, vp, dp, dp, dp, dp, C.c_int, C.c_int, dp, P(E)], C.c_int),
@@ -102,4 +104,5 @@ EXPORTS = [
     "cko_probe_fp64_tflops", "cko_comm_alloc", "cko_comm_open", "cko_ctx_set_kernel_generation",
     "cko_ctx_kernel_generation_used", "cko_chunk_residual", "cko_chunk_jacobian", "cko_adjoint_chunk_solve",
     "cko_adjoint_step_sequential", "cko_fe_forward", "cko_fe_adjoint_host", "cko_ctx_set_jacobian_strategy",
+    "cko_ctx_set_structured", "cko_ctx_structured_used",
 ]

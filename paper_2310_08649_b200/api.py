@@ -210,6 +210,18 @@ class Context:
         """Kernel generation the last forward / adjoint call ran (1 or 2)."""
         return int(lib().cko_ctx_kernel_generation_used(self.h))
 
+    # bits of structured_used() (include/chunkode_b200.h CKO_SP_*)
+    SP_FWD, SP_ADJ, SP_FWD_FALLBACK, SP_ADJ_FALLBACK = 1, 2, 4, 8
+
+    def set_structured(self, on: bool) -> None:
+        """Structured-record Thomas kernels for arrow + tridiagonal blocks (the MDS chain); on by default."""
+        if lib().cko_ctx_set_structured(self.h, 1 if on else 0) != 0:
+            raise ValueError("set_structured failed")
+
+    def structured_used(self) -> int:
+        """CKO_SP_* bits of the last forward / adjoint call: which ran structured, which fell back."""
+        return int(lib().cko_ctx_structured_used(self.h))
+
     def model(self, m: Model) -> C.c_void_p:
         key = (m.kind, m.n_unit, m.width, m.n_batch, m.lane_offset, m.params.tobytes())
         dm = self._models.get(key)

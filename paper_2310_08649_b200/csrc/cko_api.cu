@@ -52,6 +52,11 @@ cko_status ok(cko_error* e) {
     if (_e != cudaSuccess)                                                                \
       return fail(err, CKO_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));        \
   } while (0)
+#define CUDA_TRY_RAW(expr)           \
+  do {                               \
+    const cudaError_t _e = (expr);   \
+    if (_e != cudaSuccess) return _e; \
+  } while (0)
 
 struct Buf {
   void* p = nullptr;
@@ -163,7 +168,7 @@ struct cko_ctx {
   cudaEvent_t fwd_done = nullptr;
   int sms = 0;
   // workspace pool
-  Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status;
+  Buf slab, piv, rn, r0, iters, gs, key, info, loss, scratch, lambda, wq, vjp, grad, status, spfb;
   Buf lpart;       // the last forward's per-CTA sums of y^2 (the fused Frobenius loss)
   Buf feed;        // streamed time grid: rows resident (tag + rows, written by the copy stream)
   const unsigned long long* feed_ready = nullptr;  // set for the next forward_core only
@@ -183,6 +188,13 @@ struct cko_ctx {
   double last_ms[4] = {0, 0, 0, 0};
   int last_launches = 0;
   int last_gen = 0;  // kernel generation the last forward/adjoint call ran
+  // structured-record kernels (cko_sparse.cuh) for models with the arrow + tridiagonal block pattern:
+  // on by default (CKO_STRUCTURED=0 or cko_ctx_set_structured(ctx, 0) turns them off)
+  int structured = [] {
+    const char* v = std::getenv("CKO_STRUCTURED");
+    return (v && v[0] == '0') ? 0 : 1;
+  }();
+  int last_sp = 0;  // CKO_SP_* bits of the last forward / adjoint call
   void mark(int i) {
     if (timing) cudaEventRecord(ev[i], stream);
   }
@@ -294,6 +306,14 @@ cko_status cko_ctx_set_kernel_generation(cko_ctx* c, int gen) {
 }
 
 int cko_ctx_kernel_generation_used(cko_ctx* c) { return c ? c->last_gen : 0; }
+
+cko_status cko_ctx_set_structured(cko_ctx* c, int on) {
+  if (!c || (on != 0 && on != 1)) return CKO_ERROR;
+  c->structured = on;
+  return CKO_OK;
+}
+
+int cko_ctx_structured_used(cko_ctx* c) { return c ? c->last_sp : 0; }
 
 cko_status cko_ctx_set_jacobian_strategy(cko_ctx* c, int strategy) {
   if (!c || strategy < CKO_JACOBIAN_ANALYTIC || strategy > CKO_JACOBIAN_FINITE_DIFFERENCE) return CKO_ERROR;
@@ -677,26 +697,39 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
     c->last_launches = 1 + 6 * (int)n_chunks;
     c->last_gen = 2;
   } else {
-  c->mark(0);
-  if (v2)
-    CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
-  else if (p2)
-    CUDA_TRY(launch_forward_pcr2(m->dm.kind, n, &a, c->stream));
-  else
-    CUDA_TRY(launch_forward(a, c->stream));
-  c->mark(1);
-  c->last_launches = 1;
-  c->last_gen = (v2 || p2) ? 2 : 1;
-  CUDA_TRY(c->pin.ensure(32 + sizeof(int) * (size_t)n_chunks));
-  CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(0), c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(32), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
-                           c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  std::memcpy(info, c->pin.as<int>(0), sizeof info);
-  key = *c->pin.as<unsigned long long>(16);
-  c->iters_host.assign(c->pin.as<int>(32), c->pin.as<int>(32) + n_chunks);
+  c->last_sp = 0;
+  a.structured = v2 && c->structured;
+  for (int attempt = 0;; ++attempt) {
+    if (attempt > 0) {  // the structured kernels met a block they cannot factor: the group-LU kernels re-run it
+      CUDA_TRY(cudaMemsetAsync(c->gs.p, 0, offsetof(GridSync, ext_gen), c->stream));
+      CUDA_TRY(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+      CUDA_TRY(cudaMemsetAsync(c->info.p, 0, sizeof(int) * 4, c->stream));
+      a.structured = 0;
+      c->last_sp |= CKO_SP_FWD_FALLBACK;
+    }
+    c->mark(0);
+    if (v2)
+      CUDA_TRY(launch_forward_v2(m->dm.kind, n, &a, c->stream));
+    else if (p2)
+      CUDA_TRY(launch_forward_pcr2(m->dm.kind, n, &a, c->stream));
+    else
+      CUDA_TRY(launch_forward(a, c->stream));
+    c->mark(1);
+    c->last_launches = attempt + 1;
+    c->last_gen = (v2 || p2) ? 2 : 1;
+    CUDA_TRY(c->pin.ensure(32 + sizeof(int) * (size_t)n_chunks));
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(0), c->info.p, sizeof info, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<unsigned long long>(16), c->key.p, sizeof key, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->pin.as<int>(32), c->iters.p, sizeof(int) * n_chunks, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    std::memcpy(info, c->pin.as<int>(0), sizeof info);
+    key = *c->pin.as<unsigned long long>(16);
+    c->iters_host.assign(c->pin.as<int>(32), c->pin.as<int>(32) + n_chunks);
+    if (!(info[0] == 5 && a.structured)) break;
+  }
+  if (a.structured) c->last_sp |= CKO_SP_FWD;
   }
   if (a.trace) {
     std::vector<unsigned long long> h(tbuf.bytes / sizeof(unsigned long long));
@@ -854,6 +887,13 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   a.sing_key = c->key.as<unsigned long long>();
   a.grid = G;
   a.threads = kThreads;
+  c->last_sp &= CKO_SP_FWD | CKO_SP_FWD_FALLBACK;  // keep the forward's bits of a gradient_adjoint call
+  if (v2 && c->structured) {
+    CUDA_TRY(c->spfb.ensure(sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(c->spfb.p, 0, sizeof(unsigned), c->stream));
+    a.structured = 1;
+    a.sp_fallback = c->spfb.as<unsigned>();
+  }
   c->mark(2);
   if (nodep)
     CUDA_TRY(node_adjoint(m->dm, d_states, d_times, a.dL, a.loss, nb, nt, nc, c->slab.as<double>(),
@@ -868,6 +908,29 @@ cko_status adjoint_core(cko_ctx* c, const cko_model* m, const double* d_states, 
   c->mark(4);
   CUDA_TRY(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),
                       c->grad.as<double>(), c->stream));
+  // structured adjoint: a block it cannot factor makes this rank re-run the adjoint and the VJP on the
+  // group-LU kernels before anything is exchanged or read
+  auto adjoint_fallback = [&]() -> cudaError_t {
+    unsigned fb = 0;
+    cudaError_t e = cudaMemcpyAsync(c->pin.as<unsigned>(0), c->spfb.p, sizeof fb, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return e;
+    fb = *c->pin.as<unsigned>(0);
+    if (!fb) return cudaSuccess;
+    a.structured = 0;
+    c->last_sp |= CKO_SP_ADJ_FALLBACK;
+    CUDA_TRY_RAW(cudaMemsetAsync(c->key.p, 0xff, sizeof(unsigned long long), c->stream));
+    CUDA_TRY_RAW(launch_adjoint_v2(m->dm.kind, n, &a, c->stream));
+    CUDA_TRY_RAW(launch_vjp(m->dm, d_states, d_times, c->wq.as<double>(), nb, nt, c->vjp.as<double>(),
+                            c->grad.as<double>(), c->stream));
+    c->last_launches += 2;
+    return cudaSuccess;
+  };
+  if (a.structured) {
+    CUDA_TRY(c->pin.ensure(32 + sizeof(double) * (size_t)(np + 1)));
+    CUDA_TRY(adjoint_fallback());
+    if (a.structured) c->last_sp |= CKO_SP_ADJ;
+  }
   if (c->grp.world > 1) {
     CUDA_TRY(launch_key_flag(c->key.as<unsigned long long>(), c->grad.as<double>() + np, c->stream));
     CUDA_TRY(launch_group_sum(c->grp, c->gs.as<GridSync>(), c->grad.as<double>(), np + 1, c->status.as<unsigned>(),

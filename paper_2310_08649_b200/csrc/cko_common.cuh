@@ -99,6 +99,7 @@ enum : unsigned {
   FLAG_NON_FINITE = 2u,     // some lane's residual norm is not finite
   FLAG_SINGULAR = 4u,       // a diagonal block failed the pivot check
   FLAG_TIMEOUT = 8u,        // barrier wait exceeded its budget (abort)
+  FLAG_FALLBACK = 16u,      // a structured-record block is not eligible: re-run on the group-LU kernels
 };
 
 // Grid barrier state (device memory, zero-initialised by the host).

@@ -52,6 +52,8 @@ struct FwdLaunch {
   unsigned long long times_tag;
   int grid;               // CTAs
   int threads;
+  int structured;         // 1: structured-record kernels where the model has them (cko_sparse.cuh);
+                          // info[0] = 5 asks the caller to re-run with 0
 };
 
 struct AdjLaunch {
@@ -72,6 +74,8 @@ struct AdjLaunch {
   unsigned long long* sing_key;  // min over (chunk ordinal, r, b)
   int grid;
   int threads;
+  int structured;          // as FwdLaunch::structured; an ineligible block sets *sp_fallback
+  unsigned* sp_fallback;
 };
 
 struct SolveLaunch {

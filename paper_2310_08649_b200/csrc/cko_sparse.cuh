@@ -1,0 +1,399 @@
+// cko_sparse.cuh — structured Thomas epochs for the mass-damper-spring chain
+// (included by cko_v2.cuh; the kernels fwd2_kernel / adj2_kernel select them
+// with their SP template flag).
+//
+// The block of a chunk row is M = I - dt J (forward) or its transpose
+// (adjoint). The MDS Jacobian (models_mds.cpp:54-82) has a fixed pattern:
+// position row u holds J[u][NU+u] = 1, velocity row NU+u holds columns
+// u-1..u+1 and NU+u-1..NU+u+1. So, in 2x2 blocks of NU x NU,
+//     M = [ I   B ]      B, C: one or three diagonals, D: tridiagonal,
+//         [ C   D ]
+// and every other entry is an exact zero. lu_factor_block (linalg.cpp:13-44)
+// on such a block, whenever it does not exchange rows, does exactly this:
+//   * columns 0..NU-1: the pivot is M[c][c] = 1 exactly, so inv = 1 and the
+//     multipliers are C's entries unchanged; each row NU+v is updated only on
+//     the (tridiagonal) entries that row c of B reaches: D' = D - C B, one
+//     update per entry, in the same column order as the dense loop;
+//   * columns NU..N-1: LU of the tridiagonal D' (one multiplier per column).
+// Every update the dense loop applies beyond these is `x -= l * 0` or skipped
+// by its own `if (l != 0.0)`: exact no-ops for finite entries. The factors
+// (and the substitution of lu_solve_vec, linalg.cpp:46-60, over the nonzero
+// terms in the same order) are therefore the dense ones, at ~14 NU doubles
+// per record instead of N^2 and a few hundred flops instead of ~N^3 / 3.
+//
+// Eligibility is checked per block, exactly as the reference's scan decides:
+// a row exchange (some |a(r, c)| > |pivot| below the diagonal), a pivot under
+// the singularity threshold 1e-14 max|M|, or a non-finite entry makes the
+// block ineligible. The kernels then raise FLAG_FALLBACK (forward: through the
+// grid barrier, so every CTA and rank stops at the same iteration; adjoint: a
+// device word) and the host re-runs the call on the dense group-LU kernels,
+// which reproduce the reference's pivoting and singular-block reports.
+#pragma once
+
+namespace cko {
+namespace v2 {
+
+template <class MS, class = void>
+struct HasArrowTri {
+  static constexpr bool value = false;
+};
+template <class MS>
+struct HasArrowTri<MS, std::void_t<decltype(MS::kArrowTri)>> {
+  static constexpr bool value = MS::kArrowTri;
+};
+
+// Structured record (doubles). LC / UB: the C / B entries of row u at
+// columns u-1, u, u+1 of their block (3 per row; unused slots never read),
+// TL: D' multipliers (row NU+u, column NU+u-1), TD / TR / TE: U diagonal,
+// its reciprocal, superdiagonal of the velocity rows. The stride is odd so
+// 8-byte accesses of consecutive records spread over all banks.
+template <int NU>
+struct SpRec {
+  static constexpr int N = 2 * NU;
+  static constexpr int RHS = 0;
+  static constexpr int Y = N;
+  static constexpr int DT = 2 * N;
+  static constexpr int LC = DT + 1;
+  static constexpr int UB = LC + 3 * NU;
+  static constexpr int TL = UB + 3 * NU;
+  static constexpr int TD = TL + NU;
+  static constexpr int TR = TD + NU;
+  static constexpr int TE = TR + NU;
+  static constexpr int RAW = TE + NU;
+  static constexpr int STRIDE = RAW | 1;
+};
+
+// Which of the three B / C diagonals are structural: forward M has C on three
+// (velocity row NU+v couples to positions v-1..v+1) and B on one (J[u][NU+u]);
+// the adjoint's M^T the other way round.
+template <bool TR>
+struct ArrowMask {
+  static constexpr bool c(int o) { return TR ? o == 1 : true; }
+  static constexpr bool b(int o) { return TR ? true : o == 1; }
+};
+
+template <int NU>
+__device__ __forceinline__ constexpr bool in_chain(int v, int o) {
+  return v + o - 1 >= 0 && v + o - 1 < NU;
+}
+
+// Schur update D' = D - C B (columns 0..NU-1 of the elimination) and the
+// tridiagonal LU of D'. Lc, Ub: the entries of C and B; D: on entry D, on exit
+// [multiplier, U diagonal, U superdiagonal] per velocity row; rinv: 1 / U_ii.
+// mx: max |M| over the block. Returns false when lu_factor_block would pivot,
+// call the block singular, or see a non-finite value.
+template <int NU, bool TR>
+__device__ __forceinline__ bool arrow_factor(const double (&Lc)[NU][3], const double (&Ub)[NU][3], double (&D)[NU][3],
+                                             double mx, double (&rinv)[NU]) {
+  using Mk = ArrowMask<TR>;
+  const double tiny = 1e-14 * mx;
+  bool ok = mx < INFINITY && !(1.0 < tiny);  // columns 0..NU-1: the pivot is 1
+  // rows NU+v whose column c entry could beat the unit pivot (the scan's strict '>')
+#pragma unroll
+  for (int v = 0; v < NU; ++v)
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+      if (Mk::c(o) && in_chain<NU>(v, o)) ok &= !(fabs(Lc[v][o]) > 1.0);
+  // D' = D - C B: row NU+v, column c = v + oc - 1 (ascending), pivot-row entries at NU + c + ou - 1
+#pragma unroll
+  for (int v = 0; v < NU; ++v)
+#pragma unroll
+    for (int oc = 0; oc < 3; ++oc) {
+      if (!Mk::c(oc) || !in_chain<NU>(v, oc)) continue;
+      const int c = v + oc - 1;
+      const double l = Lc[v][oc];  // a(NU+v, c) * (1 / 1)
+#pragma unroll
+      for (int ou = 0; ou < 3; ++ou) {
+        if (!Mk::b(ou) || !in_chain<NU>(c, ou)) continue;
+        const int od = c + ou - 1 - v + 1;  // column NU + c + ou - 1 relative to row NU + v
+        if (od >= 0 && od < 3) D[v][od] -= l * Ub[c][ou];
+      }
+    }
+  // tridiagonal LU of D' (columns NU..N-1)
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    const double p = D[u][1];
+    const double ap = fabs(p);
+    ok &= ap >= tiny && ap != 0.0 && ap < INFINITY;
+    const double inv = 1.0 / p;
+    rinv[u] = inv;
+    if (u + 1 < NU) {
+      ok &= !(fabs(D[u + 1][0]) > ap);
+      const double l = D[u + 1][0] * inv;
+      D[u + 1][0] = l;
+      D[u + 1][1] -= l * D[u][2];
+    }
+  }
+  return ok;
+}
+
+// v <- M^{-1} v from a structured record (lu_solve_vec over the nonzero
+// terms: forward sweep j ascending, backward sweep dividing by U_ii).
+template <int NU, bool TR>
+__device__ __forceinline__ void arrow_solve(const double* __restrict__ rec, double (&x)[2 * NU]) {
+  using R = SpRec<NU>;
+  using Mk = ArrowMask<TR>;
+  // forward, unit lower: rows 0..NU-1 have no multipliers; row NU+v: C's columns, then NU+v-1
+#pragma unroll
+  for (int v = 0; v < NU; ++v) {
+    double s = x[NU + v];
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+      if (Mk::c(o) && in_chain<NU>(v, o)) s -= rec[R::LC + 3 * v + o] * x[v + o - 1];
+    if (v > 0) s -= rec[R::TL + v] * x[NU + v - 1];
+    x[NU + v] = s;
+  }
+  // backward: velocity rows (superdiagonal, then / U_ii), then position rows (B's columns; U_ii = 1)
+#pragma unroll
+  for (int v = NU - 1; v >= 0; --v) {
+    double s = x[NU + v];
+    if (v + 1 < NU) s -= rec[R::TE + v] * x[NU + v + 1];
+    x[NU + v] = div_rn(s, rec[R::TD + v], rec[R::TR + v]);
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    double s = x[u];
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+      if (Mk::b(o) && in_chain<NU>(u, o)) s -= rec[R::UB + 3 * u + o] * x[NU + u + o - 1];
+    x[u] = s;
+  }
+}
+
+// Factor and store: Lc / Ub / D hold the block's entries; the factors go to `rec`.
+template <int NU, bool TR>
+__device__ __forceinline__ bool arrow_factor_store(const double (&Lc)[NU][3], const double (&Ub)[NU][3],
+                                                   double (&D)[NU][3], double* rec) {
+  using R = SpRec<NU>;
+  using Mk = ArrowMask<TR>;
+  double mx = 1.0;  // the position rows' unit diagonal
+#pragma unroll
+  for (int v = 0; v < NU; ++v)
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (Mk::c(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Lc[v][o]));
+      if (Mk::b(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Ub[v][o]));
+      if (in_chain<NU>(v, o)) mx = fmax(mx, fabs(D[v][o]));
+    }
+  // fmax drops NaN: any NaN entry must still make the block ineligible
+  bool finite = true;
+#pragma unroll
+  for (int v = 0; v < NU; ++v)
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (Mk::c(o) && in_chain<NU>(v, o)) finite &= Lc[v][o] == Lc[v][o];
+      if (Mk::b(o) && in_chain<NU>(v, o)) finite &= Ub[v][o] == Ub[v][o];
+      if (in_chain<NU>(v, o)) finite &= D[v][o] == D[v][o];
+    }
+  double rinv[NU];
+  const bool ok = arrow_factor<NU, TR>(Lc, Ub, D, finite ? mx : INFINITY, rinv);
+#pragma unroll
+  for (int v = 0; v < NU; ++v) {
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      if (Mk::c(o) && in_chain<NU>(v, o)) rec[R::LC + 3 * v + o] = Lc[v][o];
+      if (Mk::b(o) && in_chain<NU>(v, o)) rec[R::UB + 3 * v + o] = Ub[v][o];
+    }
+    if (v > 0) rec[R::TL + v] = D[v][0];
+    rec[R::TD + v] = D[v][1];
+    rec[R::TR + v] = rinv[v];
+    if (v + 1 < NU) rec[R::TE + v] = D[v][2];
+  }
+  return ok;
+}
+
+// ---- forward epoch (one Newton iteration of one lane tile), structured records -----------------
+// Ring as in fwd_epoch (RingConsumer), with one thread per record: producer set s (one warp) fills
+// slots s, s + S, ... of RS = 32 items; the consumer warp runs one lane per thread.
+template <class MS>
+__device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, const double* cs, double* recs,
+                             const double* hr, int t0, int LTc, unsigned* s_fb) {
+  constexpr int N = MS::N, NU = N / 2;
+  using R = SpRec<NU>;
+  constexpr int kS = R::STRIDE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = sh.S, Q = sh.Q, RS = sh.RS;
+  constexpr int nthr = 64;
+  const int nb = a.nb;
+  const int pw = producer_of(warp);
+  if (pw >= 0 && pw < S) {
+    const int I = x.c * LTc, J = (I + RS - 1) / RS;
+    const double* Jm = cs + MS::JOFF;
+    for (int js = pw; js < J; js += S) {
+      const int q = js % Q;
+      const bool active = js * RS + lane < I;
+      const int item = active ? js * RS + lane : I - 1;
+      const int k = item / LTc, lb = t0 + item % LTc, b = x.lb0 + lb;
+      double* rec = recs + (size_t)(q * RS + lane) * kS;
+      // the point's iterate, residual and times are requested before the slot wait
+      const double2* yrow = reinterpret_cast<const double2*>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N);
+      const double* rrow = hr + (size_t)(k * x.L + lb) * N;  // per-CTA slab: 8-byte aligned only
+      double2 ye[NU];
+      double re[N];
+#pragma unroll
+      for (int i = 0; i < NU; ++i) ye[i] = yrow[i];
+#pragma unroll
+      for (int i = 0; i < N; ++i) re[i] = rrow[i];
+      const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
+      const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
+      if (js >= Q) bar_sync(1 + Q + q, nthr);
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+          rec[R::Y + 2 * i] = ye[i].x, rec[R::Y + 2 * i + 1] = ye[i].y;
+          rec[R::RHS + 2 * i] = re[2 * i], rec[R::RHS + 2 * i + 1] = re[2 * i + 1];
+        }
+        // M = I - dt J (the dense build's roundings: xmul(-dt, J_ij), + 1 on the diagonal)
+        const double ndt = -dt;
+        double Lc[NU][3], Ub[NU][3], D[NU][3];
+#pragma unroll
+        for (int v = 0; v < NU; ++v)
+#pragma unroll
+          for (int o = 0; o < 3; ++o) {
+            const bool in = in_chain<NU>(v, o);
+            const int cix = in ? v + o - 1 : v;
+            Lc[v][o] = in ? xmul(ndt, Jm[(NU + v) * N + cix]) : 0.0;
+            D[v][o] = in ? xmul(ndt, Jm[(NU + v) * N + NU + cix]) : 0.0;
+            Ub[v][o] = o == 1 ? xmul(ndt, Jm[v * N + NU + v]) : 0.0;
+          }
+#pragma unroll
+        for (int v = 0; v < NU; ++v) D[v][1] = xadd(D[v][1], 1.0);
+        if (!arrow_factor_store<NU, false>(Lc, Ub, D, rec)) atomicOr(s_fb, 1u);
+      }
+      bar_arrive(1 + q, nthr);
+    }
+  } else if (warp == 0) {
+    // consumer: x_k = M_k^{-1}(r_k + x_{k-1}), yy_k -= x_k, one thread per lane
+    const int lt = lane;
+    const bool active = lt < LTc;
+    const int b = x.lb0 + t0 + lt;
+    double xv[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) xv[i] = 0.0;
+    RingConsumer ring(RS, Q, LTc, x.c, nthr);
+    for (int k = 0; k < x.c; ++k) {
+      ring.acquire(k);
+      if (active) {
+        const double* rec = recs + (size_t)ring.record(k, lt) * kS;
+#pragma unroll
+        for (int i = 0; i < N; ++i) xv[i] = rec[R::RHS + i] + xv[i];
+        arrow_solve<NU, false>(rec, xv);
+        double2* yy = reinterpret_cast<double2*>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N);
+#pragma unroll
+        for (int i = 0; i < NU; ++i) yy[i] = make_double2(rec[R::Y + 2 * i] - xv[2 * i], rec[R::Y + 2 * i + 1] - xv[2 * i + 1]);
+      }
+      ring.release(k);
+    }
+  }
+}
+
+// ---- adjoint epoch (one reversed chunk of one lane tile), structured records --------------------
+template <class MS>
+__device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* cs, double* recs, double* lam,
+                             int lb0, int t0, int LTc, int step_hi, int c, double Lval, double (&dcar)[MS::N]) {
+  constexpr int N = MS::N, NU = N / 2;
+  using R = SpRec<NU>;
+  constexpr int kS = R::STRIDE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = sh.S, Q = sh.Q, RS = sh.RS;
+  constexpr int nthr = 64;
+  const int nb = a.nb;
+  const size_t row = (size_t)nb * N;
+  const int pw = producer_of(warp);
+  if (pw >= 0 && pw < S) {
+    const int I = c * LTc, J = (I + RS - 1) / RS;
+    const double* Jm = cs + MS::JOFF;
+    for (int js = pw; js < J; js += S) {
+      const int q = js % Q;
+      const bool active = js * RS + lane < I;
+      const int item = active ? js * RS + lane : I - 1;
+      const int r = item / LTc, ltc = item % LTc;
+      const int b = lb0 + t0 + ltc;
+      const int m = step_hi - r;
+      double* rec = recs + (size_t)(q * RS + lane) * kS;
+      const double* yrow = (a.dL ? a.dL : a.states) + (size_t)m * row + (size_t)b * N;
+      double yq[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) yq[i] = yrow[i];
+      const double t = a.times[(size_t)m * nb + b];
+      const double dt = t - a.times[(size_t)(m - 1) * nb + b];
+      if (js >= Q) bar_sync(1 + Q + q, nthr);
+      if (active) {
+        // rhs = dL_m + dt J^T lambda_c (gemv_transpose over J's structural nonzeros, adjoint.cpp:88-100)
+        const double* lm = lam + (size_t)ltc * N;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double dl = a.dL ? yq[i] : (Lval > 0.0 ? yq[i] / Lval : 0.0);
+          rec[R::RHS + i] = dl + dt * MS::jt_lambda(cs, i, lm);
+        }
+        rec[R::DT] = dt;
+        // M^T: B^T-side entries M[NU+u+o-1][u], C^T-side M[v][NU+v], D^T entries M[NU+v+o-1][NU+v]
+        const double ndt = -dt;
+        double Lc[NU][3], Ub[NU][3], D[NU][3];
+#pragma unroll
+        for (int v = 0; v < NU; ++v)
+#pragma unroll
+          for (int o = 0; o < 3; ++o) {
+            const bool in = in_chain<NU>(v, o);
+            const int rix = in ? v + o - 1 : v;
+            Ub[v][o] = in ? xmul(ndt, Jm[(NU + rix) * N + v]) : 0.0;
+            D[v][o] = in ? xmul(ndt, Jm[(NU + rix) * N + NU + v]) : 0.0;
+            Lc[v][o] = o == 1 ? xmul(ndt, Jm[v * N + NU + v]) : 0.0;
+          }
+#pragma unroll
+        for (int v = 0; v < NU; ++v) D[v][1] = xadd(D[v][1], 1.0);
+        if (!arrow_factor_store<NU, true>(Lc, Ub, D, rec)) atomicOr(a.sp_fallback, 1u);
+      }
+      bar_arrive(1 + q, nthr);
+    }
+  } else if (warp == 0) {
+    const int lt = lane;
+    const bool active = lt < LTc;
+    const int b = lb0 + t0 + lt;
+    const double* lc = lam + (size_t)lt * N;
+    double d[N];  // delta_{r-1}, then delta_r
+#pragma unroll
+    for (int i = 0; i < N; ++i) d[i] = 0.0;
+    RingConsumer ring(RS, Q, LTc, c, nthr);
+    for (int r = 0; r < c; ++r) {
+      ring.acquire(r);
+      if (active) {
+        const double* rec = recs + (size_t)ring.record(r, lt) * kS;
+        const int m = step_hi - r;
+#pragma unroll
+        for (int i = 0; i < N; ++i) d[i] = rec[R::RHS + i] + d[i];
+        const double dt = rec[R::DT];
+        arrow_solve<NU, true>(rec, d);
+        double* w = a.wq + (size_t)m * row + (size_t)b * N;
+#pragma unroll
+        for (int i = 0; i < N; i += 2)
+          __stcs(reinterpret_cast<double2*>(w + i), make_double2((lc[i] + d[i]) * dt, (lc[i + 1] + d[i + 1]) * dt));
+      }
+      ring.release(r);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) dcar[i] = d[i];
+  }
+}
+
+// Launch shape of the structured kernels: S one-warp producer sets, one 32-record slot each.
+template <class MS>
+inline Shape make_shape_sp(int L) {
+  constexpr int N = MS::N;
+  Shape sh;
+  sh.Ws = 1;
+  sh.RS = 32;
+  sh.S = 5;
+  sh.Q = 5;
+  sh.inv = 0;
+  sh.stride = SpRec<N / 2>::STRIDE;
+  sh.threads = 32 * kMaxWarps;
+  sh.LT = L < 32 ? L : 32;
+  int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, true);
+  sh.smem_bytes = tot * 8;
+  return sh;
+}
+
+}  // namespace v2
+}  // namespace cko

@@ -28,6 +28,8 @@ struct MdsS {
   // vector whose slices are the rows of I written as 1 / -0.0 (adding -0.0
   // leaves every off-diagonal product bit-identical).
   static constexpr bool kConstJac = true;
+  // M = I - dt J in 2 x 2 blocks: identity, one / three diagonals, tridiagonal (cko_sparse.cuh)
+  static constexpr bool kArrowTri = true;
   static constexpr int JOFF = ((2 * NU + 1) + 1) / 2 * 2;
   static constexpr int JTOFF = JOFF + N * N;
   static constexpr int ZOFF = JTOFF + N * N;

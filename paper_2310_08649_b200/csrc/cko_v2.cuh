@@ -197,12 +197,12 @@ struct Shape {
 
 template <class MS>
 __host__ __device__ inline void smem_layout(int S, int Q, int Ws, int RS, int LT, int stride, int& o_cs, int& o_rec,
-                                            int& o_pb, int& o_vs, int& o_lam, int& total_doubles) {
+                                            int& o_pb, int& o_vs, int& o_lam, int& total_doubles, bool sp = false) {
   constexpr int N = MS::N;
   o_cs = 0;
   o_rec = ((MS::NCONST + 1) / 2) * 2;
   o_pb = o_rec + Q * RS * stride;
-  const int groups = S * RS;
+  const int groups = sp ? 0 : S * RS;  // structured records (cko_sparse.cuh) need no pivot-row buffers
   o_vs = o_pb + groups * kPb<N>;
   o_lam = o_vs + LT * N + (N & 1);
   total_doubles = o_lam + LT * N + 8;
@@ -1282,20 +1282,27 @@ __device__ void fwd_epoch(const FwdLaunch& a, const FwdCtx& x, const Shape& sh, 
   }
 }
 
-template <class MS, bool INV>
+}  // namespace v2
+}  // namespace cko
+#include "cko_sparse.cuh"
+namespace cko {
+namespace v2 {
+
+// SP: the structured (arrow + tridiagonal) records of cko_sparse.cuh instead of the group LU.
+template <class MS, bool INV, bool SP = false>
 __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
   constexpr int N = MS::N;
-  constexpr int kStride = INV ? Rec<N>::STRIDE_INV : Rec<N>::STRIDE;
+  const int kStride = sh.stride;
   extern __shared__ __align__(16) double smem[];
-  __shared__ unsigned s_bcast, s_flags, s_sing;
+  __shared__ unsigned s_bcast, s_flags, s_sing, s_fb;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
   double* vss = smem + o_vs;
   MS::load_consts(a.m, cs);
-  if (threadIdx.x == 0) s_sing = 0;
+  if (threadIdx.x == 0) s_sing = 0, s_fb = 0;
   FwdCtx x;
   lane_range(a.nb, x.lb0, x.L);
   x.row = (size_t)a.nb * N;
@@ -1354,10 +1361,13 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
       ++it;
       if (ktr && it < 4) ktr[2 + 3 * (it - 1)] = globaltimer_ns();
       for (int t0 = 0; t0 < x.L; t0 += sh.LT) {
-        fwd_epoch<MS, INV>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
+        if constexpr (SP)
+          fwd_epoch_sp<MS>(a, x, sh, cs, recs, hr, t0, min(sh.LT, x.L - t0), &s_fb);
+        else
+          fwd_epoch<MS, INV>(a, x, sh, cs, recs, pbs, vss, hr, t0, min(sh.LT, x.L - t0), &s_sing);
         __syncthreads();
       }
-      const unsigned fl = s_sing ? FLAG_SINGULAR : 0u;
+      const unsigned fl = (s_sing ? FLAG_SINGULAR : 0u) | (s_fb ? FLAG_FALLBACK : 0u);
       if (ktr && it < 4) ktr[3 + 3 * (it - 1)] = globaltimer_ns();
       if (ctr && it == 1) ctr[3] = globaltimer_ns();
       f = residual2<MS>(a, x, cs, hr, nrm, recs, ring_doubles, false, &s_flags, a.loss_part ? loss_slot(a) + 1 : nullptr) | fl;
@@ -1365,9 +1375,11 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
       f = grid_reduce_or(a.gs, a.grp, f, a.budget_ns, &s_bcast);
       if (ctr && it == 1) ctr[5] = globaltimer_ns();
       if (ktr && it < 4) ktr[4 + 3 * (it - 1)] = globaltimer_ns();
-      if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE)) {
+      if (f & (FLAG_TIMEOUT | FLAG_SINGULAR | FLAG_NON_FINITE | FLAG_FALLBACK)) {
         if (leader) {
-          a.info[0] = (f & FLAG_TIMEOUT) ? 4 : (f & FLAG_SINGULAR) ? 1 : 2;
+          // a structured block the reference would pivot on (or call singular): the host re-runs the call
+          // on the group-LU kernels, whatever else this iteration saw
+          a.info[0] = (f & FLAG_TIMEOUT) ? 4 : (f & FLAG_FALLBACK) ? 5 : (f & FLAG_SINGULAR) ? 1 : 2;
           a.info[1] = step + 1;
           a.info[2] = it;
         }
@@ -1681,12 +1693,12 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
   }
 }
 
-template <class MS, bool INV>
+template <class MS, bool INV, bool SP = false>
 __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -1707,9 +1719,12 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
     while (step_hi >= 1) {
       const int c = min(a.nc, step_hi);
       double dcar[N];
-      adj_epoch<MS, INV>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
+      if constexpr (SP)
+        adj_epoch_sp<MS>(a, sh, cs, recs, lam, lb0, t0, LTc, step_hi, c, Lval, dcar);
+      else
+        adj_epoch<MS, INV>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
       __syncthreads();
-      if (INV || CKO_COOP_CONSUMER) {  // new carry (adjoint.cpp:121-126): the increments left in vss
+      if (!SP && (INV || CKO_COOP_CONSUMER)) {  // new carry (adjoint.cpp:121-126): the increments left in vss
         for (int i = threadIdx.x; i < LTc * N; i += blockDim.x) lam[i] += vss[i];
       } else if (consumer && lane < LTc) {
 #pragma unroll
@@ -1762,10 +1777,23 @@ inline Shape make_shape(int L) {
 template <class MS>
 cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
   if (!a) {  // probe: also loads the kernels (lazy module loading)
-    const cudaError_t e = preload((const void*)fwd2_kernel<MS, false>);
-    return e != cudaSuccess ? e : preload((const void*)fwd2_kernel<MS, true>);
+    cudaError_t e = preload((const void*)fwd2_kernel<MS, false>);
+    if (e == cudaSuccess) e = preload((const void*)fwd2_kernel<MS, true>);
+    if constexpr (HasArrowTri<MS>::value)
+      if (e == cudaSuccess) e = preload((const void*)fwd2_kernel<MS, false, true>);
+    return e;
   }
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
+  if constexpr (HasArrowTri<MS>::value) {
+    if (a->structured) {
+      Shape sh = make_shape_sp<MS>(Lmax);
+      const void* k = (const void*)fwd2_kernel<MS, false, true>;
+      CKO_ALLOW_FULL_SMEM(k);
+      FwdLaunch copy = *a;
+      void* args[] = {&copy, &sh};
+      return launch_persistent(k, dim3(a->grid), dim3(sh.threads), args, sh.smem_bytes, st);
+    }
+  }
   Shape sh = make_shape<MS>(Lmax);
   const void* k = sh.inv ? (const void*)fwd2_kernel<MS, true> : (const void*)fwd2_kernel<MS, false>;
   CKO_ALLOW_FULL_SMEM(k);
@@ -1777,10 +1805,21 @@ cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
 template <class MS>
 cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
   if (!a) {
-    const cudaError_t e = preload((const void*)adj2_kernel<MS, false>);
-    return e != cudaSuccess ? e : preload((const void*)adj2_kernel<MS, true>);
+    cudaError_t e = preload((const void*)adj2_kernel<MS, false>);
+    if (e == cudaSuccess) e = preload((const void*)adj2_kernel<MS, true>);
+    if constexpr (HasArrowTri<MS>::value)
+      if (e == cudaSuccess) e = preload((const void*)adj2_kernel<MS, false, true>);
+    return e;
   }
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
+  if constexpr (HasArrowTri<MS>::value) {
+    if (a->structured) {
+      const Shape sh = make_shape_sp<MS>(Lmax);
+      CKO_ALLOW_FULL_SMEM((adj2_kernel<MS, false, true>));
+      adj2_kernel<MS, false, true><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
+      return cudaGetLastError();
+    }
+  }
   Shape sh = make_shape<MS>(Lmax);
   if (sh.inv) {
     CKO_ALLOW_FULL_SMEM((adj2_kernel<MS, true>));
