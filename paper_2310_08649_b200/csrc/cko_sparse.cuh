@@ -30,6 +30,10 @@
 // which reproduce the reference's pivoting and singular-block reports.
 #pragma once
 
+#ifndef CKO_SP_DIAG
+#define CKO_SP_DIAG 0  // diagnostics only (wrong results): 1 adjoint consumer skips its stores, 2 skips the solve
+#endif
+
 namespace cko {
 namespace v2 {
 
@@ -42,25 +46,28 @@ struct HasArrowTri<MS, std::void_t<decltype(MS::kArrowTri)>> {
   static constexpr bool value = MS::kArrowTri;
 };
 
-// Structured record (doubles). LC / UB: the C / B entries of row u at
-// columns u-1, u, u+1 of their block (3 per row; unused slots never read),
-// TL: D' multipliers (row NU+u, column NU+u-1), TD / TR / TE: U diagonal,
-// its reciprocal, superdiagonal of the velocity rows. The stride is odd so
-// 8-byte accesses of consecutive records spread over all banks.
+// Structured record (doubles, 16-byte aligned pairs). C3: the entries of the
+// three-diagonal off-block (forward: C, row NU+v at columns v-1..v+1;
+// adjoint: B^T's rows) — 3 per row, chain-end slots never read; C1: the
+// one-diagonal off-block (forward: B[u][NU+u] = -dt, adjoint: C[v][v]);
+// TL: the tridiagonal multipliers (row NU+v, column NU+v-1); TR: 1 / U_ii of
+// the velocity rows; TE: their superdiagonal already scaled by 1 / U_ii.
+// The stride is 2 mod 16 doubles so the consumer threads' same-offset 16-byte
+// loads of consecutive records fall in different bank groups.
 template <int NU>
 struct SpRec {
   static constexpr int N = 2 * NU;
   static constexpr int RHS = 0;
   static constexpr int Y = N;
-  static constexpr int DT = 2 * N;
-  static constexpr int LC = DT + 1;
-  static constexpr int UB = LC + 3 * NU;
-  static constexpr int TL = UB + 3 * NU;
-  static constexpr int TD = TL + NU;
-  static constexpr int TR = TD + NU;
+  static constexpr int C3 = 2 * N;
+  static constexpr int C1 = C3 + 3 * NU;
+  static constexpr int TL = C1 + NU;
+  static constexpr int TR = TL + NU;
   static constexpr int TE = TR + NU;
-  static constexpr int RAW = TE + NU;
-  static constexpr int STRIDE = RAW | 1;
+  static constexpr int DT = TE + NU;
+  static constexpr int RAW = ((DT + 1) + 1) / 2 * 2;
+  static constexpr int STRIDE = RAW + ((2 - RAW % 16) + 16) % 16;
+  static_assert(C3 % 2 == 0 && C1 % 2 == 0 && TL % 2 == 0 && TR % 2 == 0 && TE % 2 == 0, "pairs stay aligned");
 };
 
 // Which of the three B / C diagonals are structural: forward M has C on three
@@ -127,37 +134,64 @@ __device__ __forceinline__ bool arrow_factor(const double (&Lc)[NU][3], const do
   return ok;
 }
 
-// v <- M^{-1} v from a structured record (lu_solve_vec over the nonzero
-// terms: forward sweep j ascending, backward sweep dividing by U_ii).
+template <int N>
+__device__ __forceinline__ void lds_pairs(const double* __restrict__ p, double (&v)[N]) {
+  static_assert(N % 2 == 0, "pairs");
+#pragma unroll
+  for (int i = 0; i < N; i += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(p + i);
+    v[i] = t.x, v[i + 1] = t.y;
+  }
+}
+
+// x <- M^{-1} x from a structured record: lu_solve_vec (linalg.cpp:46-60) over
+// the nonzero terms. Forward sweep as the reference (j ascending); backward
+// sweep with the row scaled by 1 / U_ii (x_i = y_i / U_ii - (U_ij / U_ii) x_j:
+// one multiply-add on the substitution chain instead of a subtract and a
+// division; rounding-level reordering of the reference's (y_i - U_ij x_j) / U_ii).
 template <int NU, bool TR>
 __device__ __forceinline__ void arrow_solve(const double* __restrict__ rec, double (&x)[2 * NU]) {
   using R = SpRec<NU>;
   using Mk = ArrowMask<TR>;
-  // forward, unit lower: rows 0..NU-1 have no multipliers; row NU+v: C's columns, then NU+v-1
+  double c3[3 * NU + (3 * NU) % 2], c1[NU + NU % 2], tl[NU + NU % 2], tr[NU + NU % 2], te[NU + NU % 2];
+  lds_pairs(rec + R::C3, c3);
+  lds_pairs(rec + R::C1, c1);
+  lds_pairs(rec + R::TL, tl);
+  lds_pairs(rec + R::TR, tr);
+  lds_pairs(rec + R::TE, te);
+  // forward, unit lower: rows 0..NU-1 have no multipliers; row NU+v: the position columns, then NU+v-1
 #pragma unroll
   for (int v = 0; v < NU; ++v) {
     double s = x[NU + v];
+    if constexpr (TR) {
+      s -= c1[v] * x[v];
+    } else {
 #pragma unroll
-    for (int o = 0; o < 3; ++o)
-      if (Mk::c(o) && in_chain<NU>(v, o)) s -= rec[R::LC + 3 * v + o] * x[v + o - 1];
-    if (v > 0) s -= rec[R::TL + v] * x[NU + v - 1];
+      for (int o = 0; o < 3; ++o)
+        if (in_chain<NU>(v, o)) s -= c3[3 * v + o] * x[v + o - 1];
+    }
+    if (v > 0) s -= tl[v] * x[NU + v - 1];
     x[NU + v] = s;
   }
-  // backward: velocity rows (superdiagonal, then / U_ii), then position rows (B's columns; U_ii = 1)
+  // backward: velocity rows, then position rows (U_ii = 1: B's columns only)
 #pragma unroll
   for (int v = NU - 1; v >= 0; --v) {
-    double s = x[NU + v];
-    if (v + 1 < NU) s -= rec[R::TE + v] * x[NU + v + 1];
-    x[NU + v] = div_rn(s, rec[R::TD + v], rec[R::TR + v]);
+    const double yv = x[NU + v] * tr[v];
+    x[NU + v] = v + 1 < NU ? fma(-te[v], x[NU + v + 1], yv) : yv;
   }
 #pragma unroll
   for (int u = 0; u < NU; ++u) {
     double s = x[u];
+    if constexpr (TR) {
 #pragma unroll
-    for (int o = 0; o < 3; ++o)
-      if (Mk::b(o) && in_chain<NU>(u, o)) s -= rec[R::UB + 3 * u + o] * x[NU + u + o - 1];
+      for (int o = 0; o < 3; ++o)
+        if (in_chain<NU>(u, o)) s -= c3[3 * u + o] * x[NU + u + o - 1];
+    } else {
+      s -= c1[u] * x[NU + u];
+    }
     x[u] = s;
   }
+  (void)Mk::c(0);
 }
 
 // Factor and store: Lc / Ub / D hold the block's entries; the factors go to `rec`.
@@ -167,40 +201,72 @@ __device__ __forceinline__ bool arrow_factor_store(const double (&Lc)[NU][3], co
   using R = SpRec<NU>;
   using Mk = ArrowMask<TR>;
   double mx = 1.0;  // the position rows' unit diagonal
+  bool finite = true;  // fmax drops NaN: any NaN entry must still make the block ineligible
 #pragma unroll
   for (int v = 0; v < NU; ++v)
 #pragma unroll
     for (int o = 0; o < 3; ++o) {
-      if (Mk::c(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Lc[v][o]));
-      if (Mk::b(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Ub[v][o]));
-      if (in_chain<NU>(v, o)) mx = fmax(mx, fabs(D[v][o]));
-    }
-  // fmax drops NaN: any NaN entry must still make the block ineligible
-  bool finite = true;
-#pragma unroll
-  for (int v = 0; v < NU; ++v)
-#pragma unroll
-    for (int o = 0; o < 3; ++o) {
-      if (Mk::c(o) && in_chain<NU>(v, o)) finite &= Lc[v][o] == Lc[v][o];
-      if (Mk::b(o) && in_chain<NU>(v, o)) finite &= Ub[v][o] == Ub[v][o];
-      if (in_chain<NU>(v, o)) finite &= D[v][o] == D[v][o];
+      if (Mk::c(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Lc[v][o])), finite &= Lc[v][o] == Lc[v][o];
+      if (Mk::b(o) && in_chain<NU>(v, o)) mx = fmax(mx, fabs(Ub[v][o])), finite &= Ub[v][o] == Ub[v][o];
+      if (in_chain<NU>(v, o)) mx = fmax(mx, fabs(D[v][o])), finite &= D[v][o] == D[v][o];
     }
   double rinv[NU];
   const bool ok = arrow_factor<NU, TR>(Lc, Ub, D, finite ? mx : INFINITY, rinv);
+  // 16-byte stores of value pairs (half the shared-memory instructions of 8-byte stores)
+  double c3[3 * NU + 1], c1[NU + 1], tl[NU + 1], tr[NU + 1], te[NU + 1];
 #pragma unroll
   for (int v = 0; v < NU; ++v) {
 #pragma unroll
-    for (int o = 0; o < 3; ++o) {
-      if (Mk::c(o) && in_chain<NU>(v, o)) rec[R::LC + 3 * v + o] = Lc[v][o];
-      if (Mk::b(o) && in_chain<NU>(v, o)) rec[R::UB + 3 * v + o] = Ub[v][o];
-    }
-    if (v > 0) rec[R::TL + v] = D[v][0];
-    rec[R::TD + v] = D[v][1];
-    rec[R::TR + v] = rinv[v];
-    if (v + 1 < NU) rec[R::TE + v] = D[v][2];
+    for (int o = 0; o < 3; ++o) c3[3 * v + o] = in_chain<NU>(v, o) ? (TR ? Ub[v][o] : Lc[v][o]) : 0.0;
+    c1[v] = TR ? Lc[v][1] : Ub[v][1];
+    tl[v] = v > 0 ? D[v][0] : 0.0;
+    tr[v] = rinv[v];
+    te[v] = v + 1 < NU ? D[v][2] * rinv[v] : 0.0;
   }
+  c3[3 * NU] = c1[NU] = tl[NU] = tr[NU] = te[NU] = 0.0;
+  auto put = [&](int off, const double* v, int n) {
+#pragma unroll
+    for (int i = 0; i < n; i += 2) *reinterpret_cast<double2*>(rec + off + i) = make_double2(v[i], v[i + 1]);
+  };
+  put(R::C3, c3, 3 * NU);
+  put(R::C1, c1, NU);
+  put(R::TL, tl, NU);
+  put(R::TR, tr, NU);
+  put(R::TE, te, NU);
   return ok;
 }
+
+// Consumer side of the ring with the structured shape's compile-time geometry (32 records per slot,
+// kSpSlots slots): RingConsumer's bookkeeping without runtime divisions.
+#ifndef CKO_SP_SLOTS
+#define CKO_SP_SLOTS 3  // knob: producer sets = slots (one warp, one 32-record slot each), barriers 1 .. 2 slots;
+                        // measured C2 adjoint ms: 7 sets 6.90, 6: 5.68, 5: 5.47, 4: 5.29, 3: 5.18 (fewer producers
+                        // contend less with the consumer; 3 still keep up)
+#endif
+constexpr int kSpSlots = CKO_SP_SLOTS;
+static_assert(kSpSlots <= 7, "named barriers 1 .. 14");
+struct RingSp {
+  int LTc, J, synced, released;
+  __device__ RingSp(int ltc, int c) : LTc(ltc), J((c * ltc + 31) >> 5), synced(0), released(0) {}
+  __device__ __forceinline__ void acquire(int k) {
+    const int need = ((k + 1) * LTc - 1) >> 5;
+    while (synced <= need) {
+      bar_sync(1 + synced % kSpSlots, 64);
+      ++synced;
+    }
+  }
+  __device__ __forceinline__ void release(int k) {
+    const int done = ((k + 1) * LTc) >> 5;
+    while (released < done) {
+      if (released + kSpSlots < J) bar_arrive(1 + kSpSlots + released % kSpSlots, 64);
+      ++released;
+    }
+  }
+  __device__ __forceinline__ int record(int k, int lane) const {
+    const int i = k * LTc + lane;
+    return ((i >> 5) % kSpSlots) * 32 + (i & 31);
+  }
+};
 
 // ---- forward epoch (one Newton iteration of one lane tile), structured records -----------------
 // Ring as in fwd_epoch (RingConsumer), with one thread per record: producer set s (one warp) fills
@@ -212,14 +278,19 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
   using R = SpRec<NU>;
   constexpr int kS = R::STRIDE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = sh.S, Q = sh.Q, RS = sh.RS;
+  constexpr int S = kSpSlots, Q = kSpSlots, RS = 32;
   constexpr int nthr = 64;
   const int nb = a.nb;
   const int pw = producer_of(warp);
+  (void)sh;
   if (pw >= 0 && pw < S) {
     const int I = x.c * LTc, J = (I + RS - 1) / RS;
     const double* Jm = cs + MS::JOFF;
+    // CKO_TRACE: slot js of the traced chunk in CTA 0: [0] wait start, [1] acquired, [2] factor start, [3] done
+    unsigned long long* tr0 = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
     for (int js = pw; js < J; js += S) {
+      unsigned long long* tr = (tr0 && js < x.c) ? tr0 + js * 8 : nullptr;
+      if (tr) tr[0] = globaltimer_ns();
       const int q = js % Q;
       const bool active = js * RS + lane < I;
       const int item = active ? js * RS + lane : I - 1;
@@ -237,11 +308,12 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
       const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
       const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
       if (js >= Q) bar_sync(1 + Q + q, nthr);
+      if (tr) tr[1] = globaltimer_ns();
       if (active) {
 #pragma unroll
-        for (int i = 0; i < NU; ++i) {
-          rec[R::Y + 2 * i] = ye[i].x, rec[R::Y + 2 * i + 1] = ye[i].y;
-          rec[R::RHS + 2 * i] = re[2 * i], rec[R::RHS + 2 * i + 1] = re[2 * i + 1];
+        for (int i = 0; i < N; i += 2) {
+          *reinterpret_cast<double2*>(rec + R::RHS + i) = make_double2(re[i], re[i + 1]);
+          *reinterpret_cast<double2*>(rec + R::Y + i) = ye[i / 2];
         }
         // M = I - dt J (the dense build's roundings: xmul(-dt, J_ij), + 1 on the diagonal)
         const double ndt = -dt;
@@ -258,8 +330,10 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
           }
 #pragma unroll
         for (int v = 0; v < NU; ++v) D[v][1] = xadd(D[v][1], 1.0);
+        if (tr) tr[2] = globaltimer_ns();
         if (!arrow_factor_store<NU, false>(Lc, Ub, D, rec)) atomicOr(s_fb, 1u);
       }
+      if (tr) tr[3] = globaltimer_ns();
       bar_arrive(1 + q, nthr);
     }
   } else if (warp == 0) {
@@ -270,18 +344,26 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
     double xv[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) xv[i] = 0.0;
-    RingConsumer ring(RS, Q, LTc, x.c, nthr);
+    unsigned long long* tr = (a.trace && blockIdx.x == 0 && x.step == trace_step(a) && lane == 0) ? a.trace + 64 : nullptr;
+    RingSp ring(LTc, x.c);
     for (int k = 0; k < x.c; ++k) {
+      if (tr) tr[k * 8 + 4] = globaltimer_ns();
       ring.acquire(k);
+      if (tr) tr[k * 8 + 5] = globaltimer_ns();
       if (active) {
         const double* rec = recs + (size_t)ring.record(k, lt) * kS;
+        double rh[N];
+        lds_pairs(rec + R::RHS, rh);
 #pragma unroll
-        for (int i = 0; i < N; ++i) xv[i] = rec[R::RHS + i] + xv[i];
+        for (int i = 0; i < N; ++i) xv[i] = rh[i] + xv[i];
         arrow_solve<NU, false>(rec, xv);
+        double yv[N];
+        lds_pairs(rec + R::Y, yv);
         double2* yy = reinterpret_cast<double2*>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N);
 #pragma unroll
-        for (int i = 0; i < NU; ++i) yy[i] = make_double2(rec[R::Y + 2 * i] - xv[2 * i], rec[R::Y + 2 * i + 1] - xv[2 * i + 1]);
+        for (int i = 0; i < NU; ++i) yy[i] = make_double2(yv[2 * i] - xv[2 * i], yv[2 * i + 1] - xv[2 * i + 1]);
       }
+      if (tr) tr[k * 8 + 6] = globaltimer_ns();
       ring.release(k);
     }
   }
@@ -289,17 +371,21 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
 
 // ---- adjoint epoch (one reversed chunk of one lane tile), structured records --------------------
 template <class MS>
-__device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* cs, double* recs, double* lam,
-                             int lb0, int t0, int LTc, int step_hi, int c, double Lval, double (&dcar)[MS::N]) {
+__device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* cs, double* recs, const double* lam,
+                             const double* jtl, int lb0, int t0, int LTc, int step_hi, int c, double Lval,
+                             double (&dcar)[MS::N]) {
+  static_assert(HasJtLambda<MS>::value, "the structured adjoint forms J^T lambda once per chunk");
   constexpr int N = MS::N, NU = N / 2;
   using R = SpRec<NU>;
   constexpr int kS = R::STRIDE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = sh.S, Q = sh.Q, RS = sh.RS;
+  constexpr int S = kSpSlots, Q = kSpSlots, RS = 32;
   constexpr int nthr = 64;
   const int nb = a.nb;
   const size_t row = (size_t)nb * N;
+  const double rL = Lval > 0.0 ? 1.0 / Lval : 0.0;
   const int pw = producer_of(warp);
+  (void)sh;
   if (pw >= 0 && pw < S) {
     const int I = c * LTc, J = (I + RS - 1) / RS;
     const double* Jm = cs + MS::JOFF;
@@ -319,12 +405,15 @@ __device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* 
       const double dt = t - a.times[(size_t)(m - 1) * nb + b];
       if (js >= Q) bar_sync(1 + Q + q, nthr);
       if (active) {
-        // rhs = dL_m + dt J^T lambda_c (gemv_transpose over J's structural nonzeros, adjoint.cpp:88-100)
-        const double* lm = lam + (size_t)ltc * N;
+        // rhs = dL_m + dt J^T lambda_c (adjoint.cpp:88-100); J^T lambda_c is the same for every row of the
+        // reversed chunk (J is constant, lambda_c is the chunk's carry): jtl, formed once per chunk
+        const double* g = jtl + (size_t)ltc * N;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          const double dl = a.dL ? yq[i] : (Lval > 0.0 ? yq[i] / Lval : 0.0);
-          rec[R::RHS + i] = dl + dt * MS::jt_lambda(cs, i, lm);
+        for (int i = 0; i < N; i += 2) {
+          // y / L from the correctly rounded 1 / L and one remainder correction (div_rn: the quotient)
+          const double d0 = a.dL ? yq[i] : (Lval > 0.0 ? div_rn(yq[i], Lval, rL) : 0.0);
+          const double d1 = a.dL ? yq[i + 1] : (Lval > 0.0 ? div_rn(yq[i + 1], Lval, rL) : 0.0);
+          *reinterpret_cast<double2*>(rec + R::RHS + i) = make_double2(d0 + dt * g[i], d1 + dt * g[i + 1]);
         }
         rec[R::DT] = dt;
         // M^T: B^T-side entries M[NU+u+o-1][u], C^T-side M[v][NU+v], D^T entries M[NU+v+o-1][NU+v]
@@ -349,25 +438,28 @@ __device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* 
   } else if (warp == 0) {
     const int lt = lane;
     const bool active = lt < LTc;
-    const int b = lb0 + t0 + lt;
-    const double* lc = lam + (size_t)lt * N;
     double d[N];  // delta_{r-1}, then delta_r
 #pragma unroll
     for (int i = 0; i < N; ++i) d[i] = 0.0;
-    RingConsumer ring(RS, Q, LTc, c, nthr);
+    const int b = lb0 + t0 + lt;
+    const double* lc = lam + (size_t)lt * N;
+    RingSp ring(LTc, c);
     for (int r = 0; r < c; ++r) {
       ring.acquire(r);
       if (active) {
-        const double* rec = recs + (size_t)ring.record(r, lt) * kS;
         const int m = step_hi - r;
+        const double* rec = recs + (size_t)ring.record(r, lt) * kS;
+        double rh[N];
+        lds_pairs(rec + R::RHS, rh);
 #pragma unroll
-        for (int i = 0; i < N; ++i) d[i] = rec[R::RHS + i] + d[i];
+        for (int i = 0; i < N; ++i) d[i] = rh[i] + d[i];
         const double dt = rec[R::DT];
-        arrow_solve<NU, true>(rec, d);
+        if (CKO_SP_DIAG != 2) arrow_solve<NU, true>(rec, d);
         double* w = a.wq + (size_t)m * row + (size_t)b * N;
 #pragma unroll
         for (int i = 0; i < N; i += 2)
-          __stcs(reinterpret_cast<double2*>(w + i), make_double2((lc[i] + d[i]) * dt, (lc[i + 1] + d[i + 1]) * dt));
+          if (CKO_SP_DIAG != 1)
+            __stcs(reinterpret_cast<double2*>(w + i), make_double2((lc[i] + d[i]) * dt, (lc[i + 1] + d[i + 1]) * dt));
       }
       ring.release(r);
     }
@@ -383,8 +475,8 @@ inline Shape make_shape_sp(int L) {
   Shape sh;
   sh.Ws = 1;
   sh.RS = 32;
-  sh.S = 5;
-  sh.Q = 5;
+  sh.S = kSpSlots;
+  sh.Q = kSpSlots;
   sh.inv = 0;
   sh.stride = SpRec<N / 2>::STRIDE;
   sh.threads = 32 * kMaxWarps;

@@ -880,7 +880,10 @@ __device__ unsigned residual2(const FwdLaunch& a, const FwdCtx& x, const double*
   int Lt = L;
   if (cap < 9 * LN + 9 * L) Lt = max(1, min(L, cap / (9 * (N + 1))));
   const int LtN = Lt * N;
-  const int KB = cap > LtN + Lt ? (cap - LtN - Lt) / (2 * LtN + Lt) : 0;  // rows per staged block
+#ifndef CKO_RES_DIRECT
+#define CKO_RES_DIRECT 0  // knob: 1 = every point straight from L2 (no shared-memory staging)
+#endif
+  const int KB = CKO_RES_DIRECT ? 0 : (cap > LtN + Lt ? (cap - LtN - Lt) / (2 * LtN + Lt) : 0);  // rows per staged block
   if (KB < 1) {  // no room to stage: one point per thread straight from L2
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       const int k = p / L, lb = p % L, b = x.lb0 + lb;
@@ -1719,10 +1722,17 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Sh
     while (step_hi >= 1) {
       const int c = min(a.nc, step_hi);
       double dcar[N];
-      if constexpr (SP)
-        adj_epoch_sp<MS>(a, sh, cs, recs, lam, lb0, t0, LTc, step_hi, c, Lval, dcar);
-      else
+      if constexpr (SP) {
+        if constexpr (HasJtLambda<MS>::value) {
+          // (J^T lambda_c)_i per lane of the tile (gemv_transpose over J's structural nonzeros, the dense sum's
+          // value), once per reversed chunk instead of per row
+          for (int e = threadIdx.x; e < LTc * N; e += blockDim.x) vss[e] = MS::jt_lambda(cs, e % N, lam + (e / N) * N);
+          __syncthreads();
+        }
+        adj_epoch_sp<MS>(a, sh, cs, recs, lam, vss, lb0, t0, LTc, step_hi, c, Lval, dcar);
+      } else {
         adj_epoch<MS, INV>(a, sh, cs, recs, pbs, vss, lam, lb0, t0, LTc, step_hi, c, Lval, ord, dcar);
+      }
       __syncthreads();
       if (!SP && (INV || CKO_COOP_CONSUMER)) {  // new carry (adjoint.cpp:121-126): the increments left in vss
         for (int i = threadIdx.x; i < LTc * N; i += blockDim.x) lam[i] += vss[i];

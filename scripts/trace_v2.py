@@ -22,10 +22,10 @@ for ch in range(4):
     row = t[ch * 16: ch * 16 + 16]
     print(ch, [(v - k0) / 1000 if v else None for v in row])
 rows = t[64:].reshape(-1, 8)
-print("row: prod(wait-start, acquired, lu-start, lu-end) cons(wait-start, acquired, done) in us")
-for k in range(min(nc, 24)):
+print("row: prod(wait-start, acquired, lu-start, lu-end) cons(wait-start, acquired, done) [writer] in us")
+for k in range(min(nc, int(os.environ.get("TRACE_ROWS", "24")))):
     r = rows[k]
-    print(k, " ".join(f"{(v - k0) / 1000:8.2f}" if v else "       -" for v in r[:7]))
+    print(k, " ".join(f"{(v - k0) / 1000:8.2f}" if v else "       -" for v in r[:8]))
 cons = rows[:, 6] - rows[:, 5]
 lu = rows[:, 3] - rows[:, 2]
 print("consumer solve us: median %.3f; producer LU us: median %.3f; producer load us: median %.3f" % (

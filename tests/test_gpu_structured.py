@@ -71,16 +71,27 @@ def test_structured_matches_group_lu(port, nb, nt, nc):
 
 @pytest.mark.parametrize("dt", [5e-5, 5e-4])
 def test_structured_falls_back_on_pivoting(port, dt):
-    """Steps large enough that the reference exchanges rows in the forward blocks: the forward must fall back
-    (the adjoint's transposed blocks pivot only at the larger step) and everything still match."""
+    """Steps large enough that the reference exchanges rows in the forward blocks (|dt K_u / M_u| > 1 below
+    the unit pivots): the forward must fall back. The adjoint's transposed blocks carry those entries in their
+    rows, not below a pivot, so it stays structured. Everything must still match."""
     m, y0, t = _mds(10, 9, 40, dt, seed=11)
     want = port.gradient(m, y0, t, 8)
     ctx = _ctx()
     got = api.gradient_adjoint(m, y0, api.TimeGrid(t), 8, ctx=ctx)
     used = ctx.structured_used()
-    assert used & api.Context.SP_FWD_FALLBACK and not used & api.Context.SP_FWD, used
-    if dt >= 5e-4:
-        assert used & api.Context.SP_ADJ_FALLBACK and not used & api.Context.SP_ADJ, used
+    assert used == api.Context.SP_FWD_FALLBACK | api.Context.SP_ADJ, used
+    _check(got, want)
+
+
+def test_structured_adjoint_falls_back(port):
+    """dt > 1: the adjoint's unit pivots are beaten by -dt below them (M^T[NU+c][c]), so the adjoint falls back
+    too."""
+    m, y0, t = _mds(2, 3, 6, 2.0, seed=4)
+    want = port.gradient(m, y0, t, 3)
+    ctx = _ctx()
+    got = api.gradient_adjoint(m, y0, api.TimeGrid(t), 3, ctx=ctx)
+    used = ctx.structured_used()
+    assert used == api.Context.SP_FWD_FALLBACK | api.Context.SP_ADJ_FALLBACK, used
     _check(got, want)
 
 
