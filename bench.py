@@ -80,17 +80,24 @@ def sweeps_per_solve(c, solver, n_switch):
     return s
 
 
-def flops_per_series_step(n, nc, solver, n_switch, k_avg):
+def flops_per_series_step(n, nc, solver, n_switch, k_avg, structured=False):
     """Algorithmic fp64 flops per series*step (MDS analytic model):
     forward: (k+1) residual passes (rate ~ 8u + 3n each) + k x [J assembly n^2,
     LU L(n), solve 2n^2 (+ PCR sweeps)], adjoint: one J^T lambda (2n^2), one LU,
     one solve (+ sweeps), quadrature + VJP (~12u). PCR adds (4n^3 + 2n^2) per
-    row per sweep beyond the first-level right solve, averaged over the chunk."""
+    row per sweep beyond the first-level right solve, averaged over the chunk.
+    structured: the arrow + tridiagonal kernels (cko_sparse.cuh) do only the
+    nonzero work of the same LU / substitution — assembly + factor ~19u,
+    substitution ~15u per block."""
     L = sum(1 + m + 2 * m * m for m in range(n))
     u = n // 2
     F_h = 8 * u + 3 * n
     sw = sweeps_per_solve(nc, solver, n_switch) / max(nc, 1)  # sweeps per row
     pcr_row = sw * (4 * n ** 3 + 2 * n * n) if solver != "thomas" else 0.0
+    if structured:
+        fwd = (k_avg + 1) * F_h + k_avg * (19 * u + 15 * u)
+        adj = 19 * u + 15 * u + 3 * n + 12 * u + 2 * n
+        return fwd + adj
     fwd = (k_avg + 1) * F_h + k_avg * (n * n + L + 2 * n * n + pcr_row)
     adj = 2 * n * n + n * n + L + 2 * n * n + pcr_row + 12 * u + 2 * n
     return fwd + adj
@@ -630,7 +637,9 @@ def main():
                  "loss_kernels": 8 * n}[dom]
     achieved = units * bytes_per / (kern[dom] * 1e-3) / 1e9
     k_avg = wf.newton_iterations / max(1, math.ceil(nt / args.n_chunk))
-    fl = flops_per_series_step(n, args.n_chunk, args.solver, args.n_switch, k_avg)
+    sp_bits = L.cko_ctx_structured_used(ctx.h) if hasattr(L, "cko_ctx_structured_used") else 0
+    structured = (sp_bits & 3) == 3  # both passes ran on the structured-record kernels
+    fl = flops_per_series_step(n, args.n_chunk, args.solver, args.n_switch, k_avg, structured)
     tf = C.c_double(0.0)
     L.cko_probe_fp64_tflops(ctx.h, C.byref(tf), C.byref(e))
     step_tflops = units * fl / (ms * 1e-3) / 1e12
@@ -646,7 +655,11 @@ def main():
         "roofline_fp64": {"bound": "fp64", "achieved": step_tflops, "peak": tf.value, "unit": "TFLOP/s",
                           "frac": step_tflops / tf.value if tf.value else None,
                           "peak_source": "measured DFMA probe (cko_probe_fp64_tflops)",
-                          "alg_flops_per_series_step": fl, "note": "whole step (fwd+adj), all kernels"},
+                          "alg_flops_per_series_step": fl,
+                          "note": "whole step (fwd+adj), all kernels" + (
+                              "; structured-record kernels: nonzero work only (the step is bound by the "
+                              "per-lane substitution chain's latency, not by FP64 or HBM throughput)"
+                              if structured else "")},
         "kernel_ms_per_step": kern,
         "newton": {"fwd": {kk: int(getattr(wf, kk)) for kk, _ in abi.CkoWork._fields_},
                    "bwd": {kk: int(getattr(wb, kk)) for kk, _ in abi.CkoWork._fields_}},
@@ -656,6 +669,8 @@ def main():
         "e2e": e2e,
     }
     line["kernel_generation"] = L.cko_ctx_kernel_generation_used(ctx.h)
+    line["structured_kernels"] = {"bits": sp_bits, "forward": bool(sp_bits & 1), "adjoint": bool(sp_bits & 2),
+                                  "fallback": bool(sp_bits & 12)}
     if ns_line is None:
         b_alg = 16 * n + 16
         ns_line = {"workload": "this run (1000 series on 1 GPU)", "value": value, "unit": "series*steps/s",

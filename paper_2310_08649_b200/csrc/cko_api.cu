@@ -587,6 +587,7 @@ cko_status forward_core(cko_ctx* c, const cko_model* m, double* d_states, const 
     slab.Lmax = (nb + G - 1) / G;
     slab.Pmax = nc_eff * slab.Lmax;
     slab.doubles = (size_t)slab.Pmax * (n + 1) + (p2 ? (size_t)slab.Pmax * pcr2_ws_bound(n) : 0);
+    slab.doubles = (slab.doubles + 1) & ~(size_t)1;  // every CTA's slab 16-byte aligned (pair loads)
     slab.ints = 0;
     CUDA_TRY(c->slab.ensure(sizeof(double) * slab.doubles * G));
     slab.base = c->slab.as<double>();

@@ -244,6 +244,11 @@ __device__ __forceinline__ bool arrow_factor_store(const double (&Lc)[NU][3], co
                         // contend less with the consumer; 3 still keep up)
 #endif
 constexpr int kSpSlots = CKO_SP_SLOTS;
+#ifndef CKO_SP_WARPS
+#define CKO_SP_WARPS 8  // knob: warps of the structured kernels (up to 255 registers per thread at 8: no spills)
+#endif
+constexpr int kSpWarps = CKO_SP_WARPS;
+static_assert(kSpWarps >= 4 && kSpWarps <= kMaxWarps, "consumer + producer warps");
 static_assert(kSpSlots <= 7, "named barriers 1 .. 14");
 struct RingSp {
   int LTc, J, synced, released;
@@ -298,13 +303,10 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
       double* rec = recs + (size_t)(q * RS + lane) * kS;
       // the point's iterate, residual and times are requested before the slot wait
       const double2* yrow = reinterpret_cast<const double2*>(a.states + (size_t)(x.step + 1 + k) * x.row + (size_t)b * N);
-      const double* rrow = hr + (size_t)(k * x.L + lb) * N;  // per-CTA slab: 8-byte aligned only
-      double2 ye[NU];
-      double re[N];
+      const double2* rrow = reinterpret_cast<const double2*>(hr + (size_t)(k * x.L + lb) * N);  // slabs: even
+      double2 ye[NU], re[NU];
 #pragma unroll
-      for (int i = 0; i < NU; ++i) ye[i] = yrow[i];
-#pragma unroll
-      for (int i = 0; i < N; ++i) re[i] = rrow[i];
+      for (int i = 0; i < NU; ++i) ye[i] = yrow[i], re[i] = rrow[i];
       const double t = a.times[(size_t)(x.step + 1 + k) * nb + b];
       const double dt = t - a.times[(size_t)(x.step + k) * nb + b];
       if (js >= Q) bar_sync(1 + Q + q, nthr);
@@ -312,7 +314,7 @@ __device__ void fwd_epoch_sp(const FwdLaunch& a, const FwdCtx& x, const Shape& s
       if (active) {
 #pragma unroll
         for (int i = 0; i < N; i += 2) {
-          *reinterpret_cast<double2*>(rec + R::RHS + i) = make_double2(re[i], re[i + 1]);
+          *reinterpret_cast<double2*>(rec + R::RHS + i) = re[i / 2];
           *reinterpret_cast<double2*>(rec + R::Y + i) = ye[i / 2];
         }
         // M = I - dt J (the dense build's roundings: xmul(-dt, J_ij), + 1 on the diagonal)
@@ -399,8 +401,16 @@ __device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* 
       double* rec = recs + (size_t)(q * RS + lane) * kS;
       const double* yrow = (a.dL ? a.dL : a.states) + (size_t)m * row + (size_t)b * N;
       double yq[N];
+      if ((reinterpret_cast<uintptr_t>(a.dL) & 15) == 0) {  // the trajectory (or an aligned user dL): pairs
 #pragma unroll
-      for (int i = 0; i < N; ++i) yq[i] = yrow[i];
+        for (int i = 0; i < N; i += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(yrow + i);
+          yq[i] = v.x, yq[i + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) yq[i] = yrow[i];
+      }
       const double t = a.times[(size_t)m * nb + b];
       const double dt = t - a.times[(size_t)(m - 1) * nb + b];
       if (js >= Q) bar_sync(1 + Q + q, nthr);
@@ -470,7 +480,7 @@ __device__ void adj_epoch_sp(const AdjLaunch& a, const Shape& sh, const double* 
 
 // Launch shape of the structured kernels: S one-warp producer sets, one 32-record slot each.
 template <class MS>
-inline Shape make_shape_sp(int L) {
+inline Shape make_shape_sp(int L, bool stage_residuals) {
   constexpr int N = MS::N;
   Shape sh;
   sh.Ws = 1;
@@ -479,10 +489,16 @@ inline Shape make_shape_sp(int L) {
   sh.Q = kSpSlots;
   sh.inv = 0;
   sh.stride = SpRec<N / 2>::STRIDE;
-  sh.threads = 32 * kMaxWarps;
+  sh.threads = 32 * kSpWarps;
   sh.LT = L < 32 ? L : 32;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, true);
+  // the record region takes the rest of shared memory: the forward's residual passes stage through it
+  // (more trajectory rows per staged block, fewer blocks per pass)
+  sh.ring = sh.Q * sh.RS * sh.stride;
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, true, sh.ring);
+  const int spare = kSmemCap / 8 - tot - 8;
+  if (stage_residuals && spare > 0) sh.ring += spare & ~1;
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, true, sh.ring);
   sh.smem_bytes = tot * 8;
   return sh;
 }

@@ -193,15 +193,17 @@ struct Shape {
   int smem_bytes;
   int inv;             // records carry M^{-1} and the consumer multiplies (few lanes per CTA)
   int stride;          // record stride in doubles (Rec<N>::STRIDE or STRIDE_INV)
+  int ring;            // doubles of the record region (>= Q RS stride; the residual passes stage through it)
 };
 
 template <class MS>
 __host__ __device__ inline void smem_layout(int S, int Q, int Ws, int RS, int LT, int stride, int& o_cs, int& o_rec,
-                                            int& o_pb, int& o_vs, int& o_lam, int& total_doubles, bool sp = false) {
+                                            int& o_pb, int& o_vs, int& o_lam, int& total_doubles, bool sp = false,
+                                            int ring = -1) {
   constexpr int N = MS::N;
   o_cs = 0;
   o_rec = ((MS::NCONST + 1) / 2) * 2;
-  o_pb = o_rec + Q * RS * stride;
+  o_pb = o_rec + (ring >= 0 ? ring : Q * RS * stride);
   const int groups = sp ? 0 : S * RS;  // structured records (cko_sparse.cuh) need no pivot-row buffers
   o_vs = o_pb + groups * kPb<N>;
   o_lam = o_vs + LT * N + (N & 1);
@@ -1293,13 +1295,13 @@ namespace v2 {
 
 // SP: the structured (arrow + tridiagonal) records of cko_sparse.cuh instead of the group LU.
 template <class MS, bool INV, bool SP = false>
-__global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
+__global__ void __launch_bounds__(SP ? 32 * kSpWarps : 32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Shape sh) {
   constexpr int N = MS::N;
   const int kStride = sh.stride;
   extern __shared__ __align__(16) double smem[];
   __shared__ unsigned s_bcast, s_flags, s_sing, s_fb;
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP, sh.ring);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -1311,7 +1313,8 @@ __global__ void __launch_bounds__(32 * kMaxWarps, 1) fwd2_kernel(FwdLaunch a, Sh
   x.row = (size_t)a.nb * N;
   double* hr = a.slab.base + (size_t)blockIdx.x * a.slab.doubles;
   // residual staging: the record ring (idle between epochs)
-  const int ring_doubles = sh.Q * sh.RS * kStride;
+  const int ring_doubles = sh.ring;
+  (void)kStride;
   double* nrm = hr + (size_t)a.slab.Pmax * N;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   __syncthreads();
@@ -1697,11 +1700,11 @@ __device__ void adj_epoch(const AdjLaunch& a, const Shape& sh, const double* cs,
 }
 
 template <class MS, bool INV, bool SP = false>
-__global__ void __launch_bounds__(32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Shape sh) {
+__global__ void __launch_bounds__(SP ? 32 * kSpWarps : 32 * kMaxWarps, 1) adj2_kernel(AdjLaunch a, Shape sh) {
   constexpr int N = MS::N;
   extern __shared__ __align__(16) double smem[];
   int o_cs, o_rec, o_pb, o_vs, o_lam, tot;
-  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP);
+  smem_layout<MS>(sh.S, sh.Q, sh.Ws, sh.RS, sh.LT, sh.stride, o_cs, o_rec, o_pb, o_vs, o_lam, tot, SP, sh.ring);
   double* cs = smem + o_cs;
   double* recs = smem + o_rec;
   double* pbs = smem + o_pb;
@@ -1780,6 +1783,7 @@ inline Shape make_shape(int L) {
     }
     if (tot * 8 <= kSmemCap || sh.inv == 0) break;
   }
+  sh.ring = sh.Q * sh.RS * sh.stride;
   sh.smem_bytes = tot * 8;
   return sh;
 }
@@ -1796,7 +1800,7 @@ cudaError_t fwd2_launch(const FwdLaunch* a, cudaStream_t st) {
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   if constexpr (HasArrowTri<MS>::value) {
     if (a->structured) {
-      Shape sh = make_shape_sp<MS>(Lmax);
+      Shape sh = make_shape_sp<MS>(Lmax, true);
       const void* k = (const void*)fwd2_kernel<MS, false, true>;
       CKO_ALLOW_FULL_SMEM(k);
       FwdLaunch copy = *a;
@@ -1824,7 +1828,7 @@ cudaError_t adj2_launch(const AdjLaunch* a, cudaStream_t st) {
   const int Lmax = (a->nb + a->grid - 1) / a->grid;
   if constexpr (HasArrowTri<MS>::value) {
     if (a->structured) {
-      const Shape sh = make_shape_sp<MS>(Lmax);
+      const Shape sh = make_shape_sp<MS>(Lmax, false);
       CKO_ALLOW_FULL_SMEM((adj2_kernel<MS, false, true>));
       adj2_kernel<MS, false, true><<<a->grid, sh.threads, sh.smem_bytes, st>>>(*a, sh);
       return cudaGetLastError();
