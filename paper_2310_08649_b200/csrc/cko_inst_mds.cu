@@ -62,12 +62,18 @@ __global__ void __launch_bounds__(256, CKO_VJP_MINB)
   const double* C = prm + NU;
   const double* M = prm + 2 * NU;
   const double fa = prm[3 * NU];
+  // x / M_j, x / M_j^2 and x / T_b from correctly rounded reciprocals plus one remainder correction
+  // (v2::div_rn, Markstein): the quotients without the divide sequence
+  double rM[NU], M2[NU], rM2[NU];
+#pragma unroll
+  for (int j = 1; j < NU; ++j) rM[j] = 1.0 / M[j], M2[j] = M[j] * M[j], rM2[j] = 1.0 / M2[j];
   double acc[NA];
 #pragma unroll
   for (int q = 0; q < NA; ++q) acc[q] = 0.0;
   const size_t row = (size_t)nb * N;
   for (int b = tid; b < nb; b += T) {
     const double Tb = m.p[3 * NU + 1 + m.off + b];
+    const double rTb = 1.0 / Tb;
     double gT = 0.0;
     for (int mm = 1 + blockIdx.x; mm <= nt; mm += gridDim.x) {
       const double* y = states + (size_t)mm * row + (size_t)b * N;
@@ -88,15 +94,15 @@ __global__ void __launch_bounds__(256, CKO_VJP_MINB)
       for (int j = 1; j < NU; ++j) {
         const double om = wv[j] - wv[j - 1];
         const double dd = yv[j] - yv[j - 1], dv = yv[NU + j] - yv[NU + j - 1];
-        acc[3 * (j - 1)] += om * dd / M[j];
-        acc[3 * (j - 1) + 1] += om * dv / M[j];
-        acc[3 * (j - 1) + 2] += -(om * (K[j] * dd + C[j] * dv) / (M[j] * M[j]));
+        acc[3 * (j - 1)] += v2::div_rn(om * dd, M[j], rM[j]);
+        acc[3 * (j - 1) + 1] += v2::div_rn(om * dv, M[j], rM[j]);
+        acc[3 * (j - 1) + 2] += -v2::div_rn(om * (K[j] * dd + C[j] * dv), M2[j], rM2[j]);
       }
-      const double ph = CKO_TWO_PI * t / Tb;
+      const double ph = v2::div_rn(CKO_TWO_PI * t, Tb, rTb);
       double s, c;
       sincos(ph, &s, &c);
       acc[NA - 1] += wv[0] * s;
-      gT += wv[0] * fa * c * (-ph / Tb);
+      gT += wv[0] * fa * c * (-v2::div_rn(ph, Tb, rTb));
     }
     prow[3 * NU + 1 + m.off + b] = gT;
   }
