@@ -52,19 +52,20 @@ def _run_group(full, nb_local, world, y0, t_local, nc, solver):
 def _run_group_once(full, nb_local, world, y0, t_local, nc, solver):
     ctxs = [api.Context(0) for _ in range(world)]
     shards = [full.shard(r * nb_local) for r in range(world)]
-    grid = api.TimeGrid(t_local)
+    grids = [api.TimeGrid(t) for t in t_local] if isinstance(t_local, list) else [api.TimeGrid(t_local)] * world
     sv = api.SolverChoice(*solver)
     # allocate every buffer first (world 1), so the concurrent runs never free / grow device memory
     for r in range(world):
-        api.gradient_adjoint(shards[r], y0[r * nb_local:(r + 1) * nb_local], grid, nc, solver=sv, ctx=ctxs[r])
+        api.gradient_adjoint(shards[r], y0[r * nb_local:(r + 1) * nb_local], grids[r], nc, solver=sv, ctx=ctxs[r])
     _group(ctxs)
     os.environ["CKO_PLAIN_LAUNCH"] = "1"  # two ranks' grids concurrently on one GPU (see cko_common.cuh)
     out, errs = [None] * world, [None] * world
 
     def rank(r):
         try:
-            out[r] = api.gradient_adjoint(shards[r], y0[r * nb_local:(r + 1) * nb_local], grid, nc, solver=sv,
+            out[r] = api.gradient_adjoint(shards[r], y0[r * nb_local:(r + 1) * nb_local], grids[r], nc, solver=sv,
                                           ctx=ctxs[r])
+            out[r].sp_bits = ctxs[r].structured_used()
         except Exception as ex:  # surfaced below
             errs[r] = ex
 
@@ -111,4 +112,26 @@ def test_two_ranks_mds_sequential_edge(port):
         cols = slice(r * nb_local * 20, (r + 1) * nb_local * 20)
         assert g.trajectory.work.as_dict() == want.fwd
         assert rel_max(g.trajectory.states, want.states[:, cols]) <= TOL
+        assert rel_max(g.gradient, want.grad) <= TOL
+
+
+def test_two_ranks_structured_fallback_on_one_rank(port):
+    """Structured MDS kernels in a group: one lane of rank 1 has steps at which the reference pivots. Its
+    forward raises the fallback flag; the group exchange carries it, so BOTH ranks stop at the same iteration
+    and re-run on the group-LU kernels (no rank waits on a peer that left). Results match the oracle on the
+    full batch."""
+    world, nb_local, nt, nc = 2, 4, 24, 6
+    full = P.build_mass_damper_spring(10, nb_local * world)
+    y0 = np.random.default_rng(5).uniform(-1e-3, 1e-3, (nb_local * world, 20))
+    t_full = uniform_times(nt, nb_local * world, nt * 1e-6)
+    t_full[:, nb_local + 2] = np.linspace(0.0, nt * 5e-4, nt + 1)  # global lane 6: rank 1's local lane 2
+    want = port.gradient(full, y0, t_full, nc)
+    t_ranks = [np.ascontiguousarray(t_full[:, r * nb_local:(r + 1) * nb_local]) for r in range(world)]
+    got = _run_group(full, nb_local, world, y0, t_ranks, nc, (0, 1))
+    for r, g in enumerate(got):
+        assert g.sp_bits & api.Context.SP_FWD_FALLBACK, (r, g.sp_bits)
+        cols = slice(r * nb_local * 20, (r + 1) * nb_local * 20)
+        assert g.trajectory.work.as_dict() == want.fwd
+        assert rel_max(g.trajectory.states, want.states[:, cols]) <= TOL
+        assert abs(g.loss - want.loss) <= TOL * abs(want.loss)
         assert rel_max(g.gradient, want.grad) <= TOL
